@@ -1,0 +1,176 @@
+"""oracle — the plain, slow, float64 CPU oracle for the linear-chain CRF hot path.
+
+TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / `--impl reference` leg may import this package.  The product
+path (paper_2002_00876_b200/) never imports it, and it never imports the product
+path.  See oracle/oracle.c for the definitions and their citations, and
+oracle/brute.py for the independent brute-force enumerator that pins it.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_lib = None
+
+F_EMPTY, F_NONFINITE, F_BADLEN = 1, 2, 4  # the documented flag contract
+LOG, MAX = 0, 1
+
+_p = ctypes.c_void_p
+_i64 = ctypes.c_int64
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so with plain gcc (no fast-math)."""
+    import subprocess
+
+    out = os.path.join(_HERE, "liboracle.so")
+    src = os.path.join(_HERE, "oracle.c")
+    if force or not os.path.exists(out) or os.path.getmtime(out) < os.path.getmtime(src):
+        subprocess.check_call(["gcc", "-O2", "-fno-fast-math", "-fPIC", "-shared", "-o", out, src,
+                               "-lm", "-lpthread"])
+    return out
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        path = os.path.join(_HERE, "liboracle.so")
+        if not os.path.exists(path):
+            build()
+        L = ctypes.CDLL(path)
+        L.oracle_semiring_matmul.argtypes = [ctypes.c_int, _p, _p, _i64, _i64, _i64, _p]
+        L.oracle_chain_marginals.argtypes = [_p, _p, _i64, _i64, _i64, _p, _p, _p, ctypes.c_int]
+        L.oracle_chain_viterbi.argtypes = [_p, _p, _i64, _i64, _i64, _p, _p, _p, ctypes.c_int]
+        L.oracle_gen_marginals.argtypes = [ctypes.c_uint64, ctypes.c_int, _i64, _i64, _i64, _p,
+                                           _i64, _p, _p, _p]
+        L.oracle_gen_viterbi.argtypes = [ctypes.c_uint64, ctypes.c_int, _i64, _i64, _i64, _p, _p,
+                                         _p]
+        L.oracle_chain_summary.argtypes = [ctypes.c_int, _p, _i64, _i64, _p]
+        L.oracle_scan_partition.argtypes = [ctypes.c_int, _p, _i64, _i64, _p, _p]
+        for f in ("oracle_semiring_matmul", "oracle_chain_marginals", "oracle_chain_viterbi",
+                  "oracle_gen_marginals", "oracle_gen_viterbi", "oracle_chain_summary",
+                  "oracle_scan_partition"):
+            getattr(L, f).restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def _f32(pot):
+    return np.ascontiguousarray(pot, dtype=np.float32)
+
+
+def _lengths(lengths, B):
+    if lengths is None:
+        return None
+    l = np.ascontiguousarray(lengths, dtype=np.int32)
+    assert l.shape == (B,)
+    return l
+
+
+def semiring_matmul(T, U, semiring: int = LOG) -> np.ndarray:
+    """V = T (x) U per §6(c), fp64."""
+    T = np.ascontiguousarray(T, dtype=np.float64)
+    U = np.ascontiguousarray(U, dtype=np.float64)
+    n, m = T.shape
+    m2, o = U.shape
+    assert m == m2
+    V = np.empty((n, o), dtype=np.float64)
+    rc = lib().oracle_semiring_matmul(semiring, T.ctypes.data, U.ctypes.data, n, m, o, V.ctypes.data)
+    assert rc == 0
+    return V
+
+
+def chain_marginals(pot, lengths=None, want_marg: bool = True, threads: int = 1):
+    """pot [B, N-1, C, C] fp32 -> (logz [B] f64, marg [B,N-1,C,C] f64 or None, flags [B] u32)."""
+    pot = _f32(pot)
+    B, E, C, C2 = pot.shape
+    assert C == C2
+    N = E + 1
+    l = _lengths(lengths, B)
+    logz = np.empty(B, dtype=np.float64)
+    marg = np.empty((B, E, C, C), dtype=np.float64) if want_marg else None
+    flags = np.zeros(B, dtype=np.uint32)
+    rc = lib().oracle_chain_marginals(pot.ctypes.data if pot.size else None,
+                                      l.ctypes.data if l is not None else None, B, N, C,
+                                      logz.ctypes.data, marg.ctypes.data if want_marg else None,
+                                      flags.ctypes.data, threads)
+    assert rc == 0
+    return logz, marg, flags
+
+
+def chain_viterbi(pot, lengths=None, threads: int = 1):
+    """-> (path [B,N] i32 with -1 beyond len, score [B] f64, flags [B] u32)."""
+    pot = _f32(pot)
+    B, E, C, _ = pot.shape
+    N = E + 1
+    l = _lengths(lengths, B)
+    path = np.empty((B, N), dtype=np.int32)
+    score = np.empty(B, dtype=np.float64)
+    flags = np.zeros(B, dtype=np.uint32)
+    rc = lib().oracle_chain_viterbi(pot.ctypes.data if pot.size else None,
+                                    l.ctypes.data if l is not None else None, B, N, C,
+                                    path.ctypes.data, score.ctypes.data, flags.ctypes.data, threads)
+    assert rc == 0
+    return path, score, flags
+
+
+def gen_marginals(seed: int, s: int, b: int, N: int, C: int, edges):
+    """Full-size sampled mode: one generated sequence b; mu at the requested edges."""
+    edges = np.ascontiguousarray(sorted(int(e) for e in edges), dtype=np.int64)
+    marg = np.empty((len(edges), C, C), dtype=np.float64)
+    logz = np.empty(1, dtype=np.float64)
+    flags = np.zeros(1, dtype=np.uint32)
+    rc = lib().oracle_gen_marginals(seed, s, b, N, C, edges.ctypes.data if len(edges) else None,
+                                    len(edges), logz.ctypes.data,
+                                    marg.ctypes.data if len(edges) else None, flags.ctypes.data)
+    assert rc == 0
+    return float(logz[0]), edges, marg, int(flags[0])
+
+
+def gen_viterbi(seed: int, s: int, b: int, N: int, C: int):
+    path = np.empty(N, dtype=np.int32)
+    score = np.empty(1, dtype=np.float64)
+    flags = np.zeros(1, dtype=np.uint32)
+    rc = lib().oracle_gen_viterbi(seed, s, b, N, C, path.ctypes.data, score.ctypes.data,
+                                  flags.ctypes.data)
+    assert rc == 0
+    return path, float(score[0]), int(flags[0])
+
+
+def chain_summary(pot_seq, semiring: int = LOG) -> np.ndarray:
+    """Transfer matrix S = l_0 (x) ... (x) l_{E-1} of one segment [E, C, C] -> [C, C] fp64."""
+    pot_seq = _f32(pot_seq)
+    E, C, _ = pot_seq.shape
+    S = np.empty((C, C), dtype=np.float64)
+    rc = lib().oracle_chain_summary(semiring, pot_seq.ctypes.data if E else None, E, C,
+                                    S.ctypes.data)
+    assert rc == 0
+    return S
+
+
+def scan_partition(pot_seq, semiring: int = LOG):
+    """Fig. 4 ordering: balanced tree with I padding. -> (root, layers)."""
+    pot_seq = _f32(pot_seq)
+    T, C, _ = pot_seq.shape
+    root = ctypes.c_double()
+    layers = ctypes.c_int()
+    rc = lib().oracle_scan_partition(semiring, pot_seq.ctypes.data, T, C, ctypes.byref(root),
+                                     ctypes.byref(layers))
+    assert rc == 0
+    return root.value, layers.value
+
+
+def max_indicator(path: np.ndarray, C: int, lengths=None) -> np.ndarray:
+    """dA*/dl as the one-hot edge indicator of the Viterbi path: [B,N-1,C,C]."""
+    B, N = path.shape
+    out = np.zeros((B, N - 1, C, C), dtype=np.float64)
+    for b in range(B):
+        n = N if lengths is None else int(lengths[b])
+        for t in range(max(n - 1, 0)):
+            if path[b, t] >= 0 and path[b, t + 1] >= 0:
+                out[b, t, path[b, t], path[b, t + 1]] = 1.0
+    return out

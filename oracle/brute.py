@@ -1,0 +1,93 @@
+"""brute.py — brute-force enumeration of every labelling z in [C]^n (TEST INFRASTRUCTURE).
+
+The second, independent witness the oracle is pinned against (PAPER.md footnote,
+P:149: "The test suite for each distribution enumerates over all structures to
+ensure that properties hold ... for small sets").  It is written against the
+structure definitions of §5.1, never the chart recursions:
+
+  Score(z) = sum_t l[t, z_t, z_{t+1}]
+  A        = log sum_z exp Score(z)
+  mu[t,i,j] = sum_{z: z_t=i, z_{t+1}=j} exp(Score(z) - A)
+  A*       = max_z Score(z)
+  z*       = the optimal labelling that is lexicographically smallest when read
+             from the last position backwards (reading R5)
+
+Guarded at C^n <= 1e6.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+GUARD = 1_000_000
+
+
+def labelings(n: int, C: int) -> np.ndarray:
+    """All C^n labelings, [C^n, n] int64 (row k = base-C digits of k, position 0 first)."""
+    count = C ** n
+    if count > GUARD:
+        raise ValueError(f"brute force refused: C^n = {count} > {GUARD}")
+    k = np.arange(count, dtype=np.int64)
+    Z = np.empty((count, n), dtype=np.int64)
+    for pos in range(n):
+        Z[:, pos] = (k // (C ** pos)) % C
+    return Z
+
+
+def scores(pot_seq: np.ndarray, n: int) -> tuple[np.ndarray, np.ndarray]:
+    """(Z, Score(z)) for the first n positions of one sequence (fp64 sums)."""
+    pot = np.asarray(pot_seq, dtype=np.float64)
+    C = pot.shape[-1]
+    Z = labelings(n, C)
+    sc = np.zeros(Z.shape[0], dtype=np.float64)
+    for t in range(n - 1):
+        sc = sc + pot[t, Z[:, t], Z[:, t + 1]]
+    return Z, sc
+
+
+def _lse(x: np.ndarray) -> float:
+    m = float(np.max(x))
+    if m == -math.inf:
+        return -math.inf
+    return m + math.log(math.fsum(np.exp(x - m).tolist()))
+
+
+def log_partition(pot_seq, n: int) -> float:
+    _, sc = scores(pot_seq, n)
+    return _lse(sc)
+
+
+def marginals(pot_seq, n: int) -> np.ndarray:
+    """mu [n-1, C, C] fp64 by direct summation over all labelings."""
+    pot = np.asarray(pot_seq, dtype=np.float64)
+    C = pot.shape[-1]
+    Z, sc = scores(pot, n)
+    A = _lse(sc)
+    mu = np.zeros((max(n - 1, 0), C, C), dtype=np.float64)
+    if A == -math.inf:
+        return mu
+    w = np.exp(sc - A)
+    for t in range(n - 1):
+        np.add.at(mu[t], (Z[:, t], Z[:, t + 1]), w)
+    return mu
+
+
+def argmax(pot_seq, n: int) -> tuple[np.ndarray, float]:
+    """(z*, A*) with the canonical tie rule R5 (reverse-lexicographic minimum)."""
+    Z, sc = scores(pot_seq, n)
+    best = float(np.max(sc))
+    opt = Z[sc == best]
+    # lexicographic order on the reversed labelling: compare z_{n-1} first, then z_{n-2}, ...
+    order = np.lexsort(opt.T)  # np.lexsort sorts by the LAST key first == position n-1 first
+    return opt[order[0]].astype(np.int32), best
+
+
+def optimal_set(pot_seq, n: int) -> np.ndarray:
+    Z, sc = scores(pot_seq, n)
+    return Z[sc == np.max(sc)]
+
+
+def count(n: int, C: int) -> int:
+    """Count semiring on zero potentials (Table 2 'Count'): |Z| = C^n."""
+    return labelings(n, C).shape[0]
