@@ -1,0 +1,162 @@
+/*
+ * ts_b200.h — C ABI of the B200-native linear-chain CRF hot path
+ * (Torch-Struct, Rush 2020, arXiv 2002.00876: PAPER.md §5.1-§6).
+ *
+ * WHAT IS COMPUTED.  A batch of B linear-chain CRFs over N positions and C labels
+ * whose parts are the edges (Table 1, "Edges (TC^2)"): the
+ * log-potential of labelling position t with i and position t+1 with j is
+ *     pot[b][t][i][j] = l(z_t = i, z_{t+1} = j),      t in [0, N-1).
+ * With Score(z) = sum_t pot[b][t][z_t][z_{t+1}]:
+ *   logZ_b      = A(l) = log sum_z exp Score(z)
+ *   marg[b][t]  = dA/dl = p(z_t=i, z_{t+1}=j)
+ *   score_b     = A*(l) = max_z Score(z);  path_b = argmax
+ * computed with the semirings of Table 2: TS_LOG = (logsumexp, +),
+ * TS_MAX = (max, +), as a chunked parallel scan of C x C semiring matrix products
+ * (§6(a), Fig. 4) with the max-shifted log product of §6(c)
+ * (P:330-331).  Marginals come from an explicit backward scan (not autodiff).
+ *
+ * Readings of the paper: no start/final/unary parts (R3: alpha_0 = 0,
+ * final (+) over all labels); Viterbi ties -> among all optimal labelings the one that
+ * is lexicographically smallest read from the last position backwards (R5);
+ * lengths: edges t >= len_b - 1 are ignored, marg = 0 and path = -1 there (R10).
+ *
+ * CONVENTIONS (all entry points).
+ *  - Every buffer is caller-owned DEVICE memory unless the name says host; the library
+ *    never allocates in a hot call and keeps no pointer after the enqueued work.
+ *  - Calls are asynchronous: work is enqueued on `stream` (a cudaStream_t; NULL = the
+ *    legacy default stream) and the call returns without synchronising.
+ *  - Synchronous errors come back as ts_status; nothing is enqueued on error:
+ *      TS_E_INVALID     null required pointer, B/N/C out of range, pot/marg not 16-byte
+ *                       aligned, other pointers not 4-byte aligned, bad semiring/op;
+ *      TS_E_UNSUPPORTED the current device is not sm_100 (B200); there is no CPU path;
+ *                       or the (semiring, C) combination is not implemented yet;
+ *      TS_E_WORKSPACE   ws_bytes < ts_workspace_bytes(...) or ws misaligned (256 B);
+ *      TS_E_CUDA        a launch or async-copy enqueue failed.
+ *  - Data-dependent conditions go to the per-sequence device `flags` array:
+ *      TS_F_EMPTY     every labelling has score -inf: logZ/score = -inf, marg = 0, path = -1;
+ *      TS_F_NONFINITE NaN or +inf on a used edge:   logZ/score = NaN,  marg = 0, path = -1;
+ *      TS_F_BADLEN    lengths[b] not in [1, N]:       logZ/score = NaN,  marg = 0, path = -1.
+ *    len_b = 1 (no edges): logZ = ln C, path = [0, -1, ...], score = 0.
+ *  - Deterministic: identical inputs give bit-identical outputs (fixed reduction orders,
+ *    no floating-point atomics).  Re-entrant: the only global state is one-time kernel
+ *    attribute setup and the debug plan knob below.
+ *  - Layouts are row-major and 64-bit indexed (B*(N-1)*C*C may exceed 2^31).
+ */
+#ifndef TS_B200_H
+#define TS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(_WIN32)
+#define TS_API
+#else
+#define TS_API __attribute__((visibility("default")))
+#endif
+
+typedef enum { TS_LOG = 0, TS_MAX = 1 } ts_semiring;
+
+typedef enum {
+  TS_OK = 0,
+  TS_E_INVALID = 1,
+  TS_E_UNSUPPORTED = 2,
+  TS_E_WORKSPACE = 3,
+  TS_E_CUDA = 4
+} ts_status;
+
+enum { TS_F_EMPTY = 1u, TS_F_NONFINITE = 2u, TS_F_BADLEN = 4u }; /* per-sequence flags */
+
+/* `op` argument of ts_workspace_bytes */
+enum {
+  TS_OP_LOGZ = 0,      /* ts_logpartition                                   */
+  TS_OP_MARG = 1,      /* ts_marginals                                      */
+  TS_OP_VITERBI = 2,   /* ts_viterbi                                        */
+  TS_OP_MARG_HOST = 3, /* ts_marginals_host (adds device staging of I/O)    */
+  TS_OP_SEGMENT = 4    /* ts_segment_summary + ts_segment_finish            */
+};
+
+/* One batch of chains.  N >= 1 positions (N-1 edges), 1 <= B, 1 <= C <= 256.
+ * pot:     [B][N-1][C][C] fp32, row-major, 16-byte aligned; pot[b][t][i][j] =
+ *          l(z_t = i, z_{t+1} = j) (reading R1: first label index = earlier position).
+ *          May be NULL only when N == 1.  -inf is a legal mask value.
+ * lengths: [B] int32 device array with values in [1, N], or NULL => every len_b = N. */
+typedef struct {
+  int64_t B, N, C;
+  const float *pot;
+  const int32_t *lengths;
+} ts_chain;
+
+/* Bytes of device workspace the given call needs (0 is possible).  Returns 0 and the
+ * call will fail with TS_E_INVALID if the chain is invalid. */
+TS_API size_t ts_workspace_bytes(const ts_chain *c, int op, ts_semiring s);
+
+/* A(l) per sequence (§5.1; TS_MAX: A*(l)).
+ * logz [B] fp32 out; flags [B] u32 out or NULL. */
+TS_API ts_status ts_logpartition(const ts_chain *c, ts_semiring s, float *logz, uint32_t *flags,
+                                 void *ws, size_t ws_bytes, void *stream);
+
+/* Marginals dA/dl for TS_LOG; for TS_MAX the one-hot indicator of the
+ * canonical argmax structure, d(A^*)/d(l).  marg [B][N-1][C][C] fp32 out
+ * (16-byte aligned); logz [B] out or NULL; flags [B] out or NULL. */
+TS_API ts_status ts_marginals(const ts_chain *c, ts_semiring s, float *marg, float *logz,
+                              uint32_t *flags, void *ws, size_t ws_bytes, void *stream);
+
+/* Viterbi argmax with backpointers (max semiring; tie rule R5).
+ * path [B][N] int32 out (-1 beyond len_b); score [B] fp32 out; flags [B] out or NULL. */
+TS_API ts_status ts_viterbi(const ts_chain *c, int32_t *path, float *score, uint32_t *flags,
+                            void *ws, size_t ws_bytes, void *stream);
+
+/* End-to-end variant of ts_marginals with HOST buffers: host_chain->pot / ->lengths and
+ * host_marg / host_logz / host_flags are host pointers (pinned for overlap); the call
+ * enqueues the H2D copies, the scan and the D2H copies on `stream` using device staging
+ * inside `ws` (size from TS_OP_MARG_HOST).  Synchronise the stream before reading. */
+TS_API ts_status ts_marginals_host(const ts_chain *host_chain, ts_semiring s, float *host_marg,
+                                   float *host_logz, uint32_t *host_flags, void *ws,
+                                   size_t ws_bytes, void *stream);
+
+/* ---- time-sharded chains (§6(a) scan across devices) --------------------
+ * A chain of n_global positions is split into contiguous segments; a rank holds edges
+ * [edge_begin, edge_begin + local->N - 1) in local->pot (local->N = local edge count + 1)
+ * for every sequence of the batch (local->lengths must be NULL: full-length chains).
+ * Step 1: ts_segment_summary writes this segment's C x C transfer matrix per sequence
+ *         (the semiring product of its edges) into `summary`, laid out as
+ *         ts_segment_summary_bytes(local) bytes: [B][C][C] fp32 log2-domain values
+ *         relative to a per-sequence fp64 scale, followed by [B] fp64 scales.
+ * Step 2: the caller all-gathers the summaries of all `world` segments, in rank order,
+ *         into all_summaries ([world] x ts_segment_summary_bytes) — e.g. NCCL
+ *         all_gather_into_tensor over NVLink.
+ * Step 3: ts_segment_finish combines them (every rank computes the same prefix/suffix
+ *         products in the same order, so logZ is bit-identical across ranks) and runs the
+ *         local forward/backward sweeps: logz [B] (global A), marg (local edges) or NULL.
+ * TS_MAX is supported for the summary/logz (score) only in this round. */
+TS_API size_t ts_segment_summary_bytes(const ts_chain *local);
+TS_API ts_status ts_segment_summary(const ts_chain *local, int64_t edge_begin, int64_t n_global,
+                                    ts_semiring s, void *summary, void *ws, size_t ws_bytes,
+                                    void *stream);
+TS_API ts_status ts_segment_finish(const ts_chain *local, int64_t edge_begin, int64_t n_global,
+                                   int rank, int world, ts_semiring s, const void *all_summaries,
+                                   float *marg_or_null, float *logz, uint32_t *flags, void *ws,
+                                   size_t ws_bytes, void *stream);
+
+/* Debug/testing plan knob (process-global): chunk length L of the time-chunked scan.
+ * 0 = automatic; 1 = the paper's pure Fig. 4 tree (every edge a leaf); >= N-1 = serial
+ * sweep (no tree).  Results agree across plans within the parity tolerances (Viterbi:
+ * bit-identical). */
+TS_API void ts_set_plan_chunk(int64_t L);
+TS_API int64_t ts_get_plan_chunk(void);
+
+/* Number of kernel launches the most recent successful call on this host thread
+ * enqueued (bench accounting). */
+TS_API int ts_last_launch_count(void);
+
+TS_API const char *ts_status_str(ts_status s);
+TS_API const char *ts_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TS_B200_H */

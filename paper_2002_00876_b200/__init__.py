@@ -1,0 +1,168 @@
+"""paper_2002_00876_b200 — B200-native linear-chain CRF hot path of Torch-Struct
+(Rush 2020, arXiv 2002.00876): log-partition A(l), marginals dA/dl and the Viterbi
+argmax, computed by hand-written sm_100a CUDA kernels behind a C ABI
+(include/ts_b200.h).  This module only marshals arguments: torch provides device
+memory and the current stream; every step of the computation runs in the kernels.
+
+    logz, flags         = logpartition(pot, lengths=None, semiring="log")
+    marg, logz, flags   = marginals(pot, lengths=None, semiring="log")
+    path, score, flags  = viterbi(pot, lengths=None)
+
+pot: float32 CUDA tensor [B, N-1, C, C] with pot[b, t, i, j] = l(z_t=i, z_{t+1}=j);
+lengths: int32 CUDA tensor [B] in [1, N] or None.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _lib
+from ._lib import TS_F_BADLEN, TS_F_EMPTY, TS_F_NONFINITE, TsError  # noqa: F401
+
+__all__ = ["logpartition", "marginals", "viterbi", "marginals_host", "set_plan_chunk",
+           "get_plan_chunk", "last_launch_count", "workspace_bytes", "Workspace", "TsError"]
+
+_SEMI = {"log": _lib.TS_LOG, "max": _lib.TS_MAX}
+
+
+def _semi(s) -> int:
+    if isinstance(s, int):
+        return s
+    return _SEMI[s]
+
+
+def _chain(pot: torch.Tensor, lengths, N: int | None = None) -> _lib.ts_chain:
+    if pot.dim() != 4 or pot.shape[2] != pot.shape[3]:
+        raise ValueError("pot must be [B, N-1, C, C]")
+    if pot.dtype != torch.float32 or not pot.is_contiguous():
+        raise ValueError("pot must be a contiguous float32 tensor")
+    B, E, C, _ = pot.shape
+    if lengths is not None:
+        if lengths.dtype != torch.int32 or lengths.shape != (B,) or lengths.device != pot.device:
+            raise ValueError("lengths must be an int32 tensor [B] on pot's device")
+    return _lib.ts_chain(B, E + 1, C, pot.data_ptr() if pot.numel() else None,
+                         lengths.data_ptr() if lengths is not None else None)
+
+
+def _stream(device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+class Workspace:
+    """Caller-owned device workspace, grown on demand (one per device)."""
+
+    _per_device: dict = {}
+
+    def __init__(self, device):
+        self.device = torch.device(device)
+        self.buf = torch.empty(0, dtype=torch.uint8, device=self.device)
+
+    @classmethod
+    def get(cls, device) -> "Workspace":
+        d = torch.device(device)
+        key = (d.type, d.index if d.index is not None else torch.cuda.current_device())
+        ws = cls._per_device.get(key)
+        if ws is None:
+            ws = cls._per_device[key] = Workspace(d)
+        return ws
+
+    def ptr(self, nbytes: int) -> int:
+        if nbytes == 0:
+            return 0
+        if self.buf.numel() < nbytes + 256:
+            self.buf = torch.empty(nbytes + 256, dtype=torch.uint8, device=self.device)
+        p = self.buf.data_ptr()
+        return (p + 255) & ~255
+
+
+def workspace_bytes(pot, lengths=None, op: int = _lib.TS_OP_MARG, semiring="log") -> int:
+    L = _lib.load()
+    ch = _chain(pot, lengths)
+    return int(L.ts_workspace_bytes(ctypes.byref(ch), op, _semi(semiring)))
+
+
+def _ws(pot, ch, op, semi, ws):
+    L = _lib.load()
+    need = int(L.ts_workspace_bytes(ctypes.byref(ch), op, semi))
+    ws = ws or Workspace.get(pot.device)
+    return ws.ptr(need), need
+
+
+def logpartition(pot: torch.Tensor, lengths=None, semiring="log", ws: Workspace | None = None):
+    """A(l) per sequence (semiring='max' gives A*(l))."""
+    L = _lib.load()
+    ch = _chain(pot, lengths)
+    semi = _semi(semiring)
+    B = pot.shape[0]
+    logz = torch.empty(B, dtype=torch.float32, device=pot.device)
+    flags = torch.empty(B, dtype=torch.int32, device=pot.device)
+    wp, wn = _ws(pot, ch, _lib.TS_OP_LOGZ, semi, ws)
+    _lib.check(L.ts_logpartition(ctypes.byref(ch), semi, logz.data_ptr(), flags.data_ptr(), wp,
+                                 wn, _stream(pot.device)), "ts_logpartition")
+    return logz, flags
+
+
+def marginals(pot: torch.Tensor, lengths=None, semiring="log", ws: Workspace | None = None,
+              out: torch.Tensor | None = None):
+    """dA/dl [B, N-1, C, C], logZ [B], flags [B]."""
+    L = _lib.load()
+    ch = _chain(pot, lengths)
+    semi = _semi(semiring)
+    B = pot.shape[0]
+    marg = out if out is not None else torch.empty_like(pot)
+    logz = torch.empty(B, dtype=torch.float32, device=pot.device)
+    flags = torch.empty(B, dtype=torch.int32, device=pot.device)
+    wp, wn = _ws(pot, ch, _lib.TS_OP_MARG, semi, ws)
+    _lib.check(L.ts_marginals(ctypes.byref(ch), semi, marg.data_ptr(), logz.data_ptr(),
+                              flags.data_ptr(), wp, wn, _stream(pot.device)), "ts_marginals")
+    return marg, logz, flags
+
+
+def viterbi(pot: torch.Tensor, lengths=None, ws: Workspace | None = None):
+    """Canonical argmax labelling (reading R5): path [B, N], score [B], flags."""
+    L = _lib.load()
+    ch = _chain(pot, lengths)
+    B, E = pot.shape[0], pot.shape[1]
+    path = torch.empty((B, E + 1), dtype=torch.int32, device=pot.device)
+    score = torch.empty(B, dtype=torch.float32, device=pot.device)
+    flags = torch.empty(B, dtype=torch.int32, device=pot.device)
+    wp, wn = _ws(pot, ch, _lib.TS_OP_VITERBI, _lib.TS_MAX, ws)
+    _lib.check(L.ts_viterbi(ctypes.byref(ch), path.data_ptr(), score.data_ptr(), flags.data_ptr(),
+                            wp, wn, _stream(pot.device)), "ts_viterbi")
+    return path, score, flags
+
+
+def marginals_host(pot_host: torch.Tensor, marg_host: torch.Tensor, logz_host: torch.Tensor,
+                   flags_host: torch.Tensor | None = None, lengths_host=None, semiring="log",
+                   device=None, ws: Workspace | None = None):
+    """End-to-end call with HOST (ideally pinned) buffers; copies happen inside the C ABI call.
+
+    Enqueued on the current stream of `device`; synchronise before reading the outputs.
+    """
+    L = _lib.load()
+    device = torch.device(device or "cuda")
+    B, E, C, _ = pot_host.shape
+    ch = _lib.ts_chain(B, E + 1, C, pot_host.data_ptr() if pot_host.numel() else None,
+                       lengths_host.data_ptr() if lengths_host is not None else None)
+    semi = _semi(semiring)
+    need = int(L.ts_workspace_bytes(ctypes.byref(ch), _lib.TS_OP_MARG_HOST, semi))
+    ws = ws or Workspace.get(device)
+    wp = ws.ptr(need)
+    _lib.check(L.ts_marginals_host(ctypes.byref(ch), semi, marg_host.data_ptr(),
+                                   logz_host.data_ptr(),
+                                   flags_host.data_ptr() if flags_host is not None else None, wp,
+                                   need, _stream(device)), "ts_marginals_host")
+
+
+def set_plan_chunk(L: int) -> None:
+    """Debug knob: 0 auto, 1 = pure Fig. 4 tree, >= N-1 = serial sweep."""
+    _lib.load().ts_set_plan_chunk(int(L))
+
+
+def get_plan_chunk() -> int:
+    return int(_lib.load().ts_get_plan_chunk())
+
+
+def last_launch_count() -> int:
+    return int(_lib.load().ts_last_launch_count())

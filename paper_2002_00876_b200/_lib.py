@@ -1,0 +1,79 @@
+"""ctypes binding of libts_b200.so (include/ts_b200.h).  Argument marshalling only.
+
+The library is built in-tree by `make` / `__graft_entry__.build()`; importing this
+module without it raises immediately — there is no CPU fallback anywhere.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libts_b200.so")
+
+TS_LOG, TS_MAX = 0, 1
+TS_OP_LOGZ, TS_OP_MARG, TS_OP_VITERBI, TS_OP_MARG_HOST, TS_OP_SEGMENT = 0, 1, 2, 3, 4
+TS_F_EMPTY, TS_F_NONFINITE, TS_F_BADLEN = 1, 2, 4
+STATUS = {0: "TS_OK", 1: "TS_E_INVALID", 2: "TS_E_UNSUPPORTED", 3: "TS_E_WORKSPACE",
+          4: "TS_E_CUDA"}
+
+# Every symbol include/ts_b200.h declares (checked by tests/test_abi_cpu.py).
+SYMBOLS = ("ts_workspace_bytes", "ts_logpartition", "ts_marginals", "ts_viterbi",
+           "ts_marginals_host", "ts_segment_summary_bytes", "ts_segment_summary",
+           "ts_segment_finish", "ts_set_plan_chunk", "ts_get_plan_chunk",
+           "ts_last_launch_count", "ts_status_str", "ts_version")
+
+
+class ts_chain(ctypes.Structure):
+    _fields_ = [("B", ctypes.c_int64), ("N", ctypes.c_int64), ("C", ctypes.c_int64),
+                ("pot", ctypes.c_void_p), ("lengths", ctypes.c_void_p)]
+
+
+class TsError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        self.status = status
+        super().__init__(f"{where}: {STATUS.get(status, status)} "
+                         f"({_lib.ts_status_str(status).decode() if _lib else ''})")
+
+
+_lib = None
+
+
+def load():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"{LIB_PATH} is missing: build the CUDA library first "
+                           "(python -c 'import __graft_entry__ as g; g.build()'); "
+                           "there is no CPU fallback")
+    L = ctypes.CDLL(LIB_PATH)
+    P, I64, SZ, INT = ctypes.c_void_p, ctypes.c_int64, ctypes.c_size_t, ctypes.c_int
+    CH = ctypes.POINTER(ts_chain)
+    L.ts_workspace_bytes.argtypes = [CH, INT, INT]
+    L.ts_workspace_bytes.restype = SZ
+    L.ts_logpartition.argtypes = [CH, INT, P, P, P, SZ, P]
+    L.ts_marginals.argtypes = [CH, INT, P, P, P, P, SZ, P]
+    L.ts_viterbi.argtypes = [CH, P, P, P, P, SZ, P]
+    L.ts_marginals_host.argtypes = [CH, INT, P, P, P, P, SZ, P]
+    L.ts_segment_summary_bytes.argtypes = [CH]
+    L.ts_segment_summary_bytes.restype = SZ
+    L.ts_segment_summary.argtypes = [CH, I64, I64, INT, P, P, SZ, P]
+    L.ts_segment_finish.argtypes = [CH, I64, I64, INT, INT, INT, P, P, P, P, P, SZ, P]
+    for f in ("ts_logpartition", "ts_marginals", "ts_viterbi", "ts_marginals_host",
+              "ts_segment_summary", "ts_segment_finish"):
+        getattr(L, f).restype = INT
+    L.ts_set_plan_chunk.argtypes = [I64]
+    L.ts_set_plan_chunk.restype = None
+    L.ts_get_plan_chunk.restype = I64
+    L.ts_last_launch_count.restype = INT
+    L.ts_status_str.argtypes = [INT]
+    L.ts_status_str.restype = ctypes.c_char_p
+    L.ts_version.restype = ctypes.c_char_p
+    _lib = L
+    return L
+
+
+def check(status: int, where: str) -> None:
+    if status != 0:
+        raise TsError(status, where)

@@ -1,0 +1,340 @@
+// abi.cu — the C ABI (include/ts_b200.h): validation, plan selection, workspace layout
+// and dispatch to the sm_100a kernels.  No CPU compute path exists: on a non-sm_100
+// device every entry point returns TS_E_UNSUPPORTED.
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+
+#include "common.cuh"
+#include "kernels.cuh"
+#include "ts_b200.h"
+
+using namespace tsb;
+
+namespace {
+
+std::atomic<int64_t> g_plan_chunk{0};
+thread_local int t_launches = 0;
+
+constexpr size_t kAlign = 256;
+inline size_t align_up(size_t x) { return (x + kAlign - 1) & ~(kAlign - 1); }
+
+// Bump allocator over the caller's workspace.
+struct Carve {
+  char* base;
+  size_t off = 0;
+  explicit Carve(void* p) : base(static_cast<char*>(p)) {}
+  template <typename T>
+  T* take(size_t n) {
+    T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+    off = align_up(off + n * sizeof(T));
+    return p;
+  }
+};
+
+bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+bool chain_ok(const ts_chain* c) {
+  if (!c) return false;
+  if (c->B < 1 || c->N < 1 || c->C < 1 || c->C > 256) return false;
+  if (c->B > (int64_t)1 << 31 || c->N > (int64_t)1 << 40) return false;
+  const double elems = (double)c->B * (double)(c->N - 1) * (double)c->C * (double)c->C;
+  if (elems > 9.0e18) return false;
+  if (c->N > 1 && (!c->pot || !aligned(c->pot, 16))) return false;
+  if (c->lengths && !aligned(c->lengths, 4)) return false;
+  return true;
+}
+
+// sm_100 (B200) check, cached per device.
+std::atomic<int> g_dev_ok[64];
+bool device_ok() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return false;
+  if (dev < 0 || dev >= 64) return false;
+  int v = g_dev_ok[dev].load();
+  if (v == 0) {
+    int maj = 0, min = 0;
+    cudaDeviceGetAttribute(&maj, cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&min, cudaDevAttrComputeCapabilityMinor, dev);
+    v = (maj == 10 && min == 0) ? 1 : 2;
+    g_dev_ok[dev].store(v);
+  }
+  return v == 1;
+}
+
+enum class Plan { Small, Stream, Unsupported };
+
+Plan log_plan(const ts_chain* c) {
+  const int64_t L = g_plan_chunk.load();
+  const int64_t E = c->N - 1;
+  const bool serial_ok = (L == 0 || L >= E);
+  if (serial_ok && small_fits(c->N, c->C)) return Plan::Small;
+  if (c->C <= 128) return Plan::Stream;
+  return Plan::Unsupported;
+}
+
+// Workspace layout of the streaming log path (P = 1).
+struct StreamWs {
+  float* alpha_hat = nullptr;
+  float* mlag = nullptr;
+  float* tmax = nullptr;
+  float* alpha_end = nullptr;
+  double* alpha_end_off = nullptr;
+  uint32_t* wflags = nullptr;
+};
+size_t stream_ws(const ts_chain* c, bool marg, void* ws, StreamWs* out) {
+  Carve cv(ws);
+  StreamWs w;
+  const int64_t B = c->B, N = c->N, C = c->C, E = N - 1;
+  if (marg) {
+    w.alpha_hat = cv.take<float>((size_t)(B * N * C));
+    w.mlag = cv.take<float>((size_t)(B * N));
+    w.tmax = cv.take<float>((size_t)(B * (E > 0 ? E : 1)));
+  }
+  w.alpha_end = cv.take<float>((size_t)(B * C));
+  w.alpha_end_off = cv.take<double>((size_t)B);
+  w.wflags = cv.take<uint32_t>((size_t)B);
+  if (out) *out = w;
+  return cv.off;
+}
+
+struct VitWs {
+  uint8_t* bp = nullptr;
+  int32_t* zend = nullptr;
+  int32_t* path = nullptr;
+  float* score = nullptr;
+};
+size_t vit_ws(const ts_chain* c, bool need_path, bool need_score, void* ws, VitWs* out) {
+  Carve cv(ws);
+  VitWs w;
+  const int64_t B = c->B, N = c->N, C = c->C, E = N - 1;
+  w.bp = cv.take<uint8_t>((size_t)(B * (E > 0 ? E : 1) * C));
+  w.zend = cv.take<int32_t>((size_t)B);
+  if (need_path) w.path = cv.take<int32_t>((size_t)(B * N));
+  if (need_score) w.score = cv.take<float>((size_t)B);
+  if (out) *out = w;
+  return cv.off;
+}
+
+size_t op_ws(const ts_chain* c, int op, ts_semiring s, void* ws, StreamWs* sw, VitWs* vw) {
+  if (s == TS_MAX) {
+    switch (op) {
+      case TS_OP_LOGZ: return vit_ws(c, false, true, ws, vw);
+      case TS_OP_MARG: return vit_ws(c, true, true, ws, vw);
+      case TS_OP_VITERBI: return vit_ws(c, false, false, ws, vw);
+      default: return 0;
+    }
+  }
+  if (op == TS_OP_VITERBI) return vit_ws(c, false, false, ws, vw);
+  const Plan p = log_plan(c);
+  if (p == Plan::Small) return 0;
+  return stream_ws(c, op == TS_OP_MARG, ws, sw);
+}
+
+ts_status cuda_status(cudaError_t e) {
+  if (e == cudaSuccess) return TS_OK;
+  cudaGetLastError();  // clear sticky launch error state where possible
+  return TS_E_CUDA;
+}
+
+ts_status run_log(const ts_chain* c, float* marg, float* logz, uint32_t* flags, void* ws,
+                  size_t ws_bytes, cudaStream_t st) {
+  const Plan p = log_plan(c);
+  if (p == Plan::Unsupported) return TS_E_UNSUPPORTED;
+  if (p == Plan::Small) {
+    SmallArgs a{c->pot, c->lengths, c->B, c->N, c->C, marg, logz, flags};
+    ts_status r = cuda_status(launch_small(a, st));
+    if (r == TS_OK) t_launches = 1;
+    return r;
+  }
+  StreamWs w;
+  const size_t need = stream_ws(c, marg != nullptr, ws, &w);
+  if (ws_bytes < need || (need && (!ws || !aligned(ws, kAlign)))) return TS_E_WORKSPACE;
+  SweepArgs a{};
+  a.pot = c->pot;
+  a.lengths = c->lengths;
+  a.B = c->B;
+  a.N = c->N;
+  a.C = c->C;
+  a.L = (c->N > 1) ? c->N - 1 : 1;
+  a.P = 1;
+  a.alpha_hat = w.alpha_hat;
+  a.alpha_end = w.alpha_end;
+  a.alpha_end_off = w.alpha_end_off;
+  a.mlag = w.mlag;
+  a.tmax = w.tmax;
+  a.marg = marg;
+  a.wflags = w.wflags;
+  a.logz = logz;
+  a.flags = flags;
+  a.final_in_fwd = marg ? 0 : 1;
+  cudaError_t e = cudaMemsetAsync(w.wflags, 0, sizeof(uint32_t) * (size_t)c->B, st);
+  if (e != cudaSuccess) return cuda_status(e);
+  e = launch_fwd(a, st);
+  if (e != cudaSuccess) return cuda_status(e);
+  int n = 1;
+  if (marg) {
+    e = launch_bwd(a, st);
+    if (e != cudaSuccess) return cuda_status(e);
+    ++n;
+  }
+  t_launches = n;
+  return TS_OK;
+}
+
+ts_status run_max(const ts_chain* c, int op, float* marg, float* logz, int32_t* path,
+                  float* score, uint32_t* flags, void* ws, size_t ws_bytes, cudaStream_t st) {
+  VitWs w;
+  const bool need_path = (op == TS_OP_MARG);
+  const size_t need = vit_ws(c, need_path, op != TS_OP_VITERBI, ws, &w);
+  if (ws_bytes < need || !ws || !aligned(ws, kAlign)) return TS_E_WORKSPACE;
+  VitArgs a{};
+  a.pot = c->pot;
+  a.lengths = c->lengths;
+  a.B = c->B;
+  a.N = c->N;
+  a.C = c->C;
+  a.bp = w.bp;
+  a.zend = w.zend;
+  a.score = score ? score : w.score;
+  a.flags = flags;
+  a.path = path ? path : w.path;
+  a.marg = marg;
+  a.logz = logz;
+  int n = 0;
+  ts_status r = cuda_status(launch_viterbi(a, st, &n));
+  if (r == TS_OK) t_launches = n;
+  return r;
+}
+
+}  // namespace
+
+extern "C" {
+
+TS_API size_t ts_workspace_bytes(const ts_chain* c, int op, ts_semiring s) {
+  if (!chain_ok(c) || (s != TS_LOG && s != TS_MAX)) return 0;
+  if (op == TS_OP_MARG_HOST) {
+    Carve cv(nullptr);
+    const int64_t B = c->B, N = c->N, C = c->C, E = N - 1;
+    cv.take<float>((size_t)(B * E * C * C));  // pot
+    cv.take<int32_t>((size_t)B);               // lengths
+    cv.take<float>((size_t)(B * E * C * C));  // marg
+    cv.take<float>((size_t)B);                 // logz
+    cv.take<uint32_t>((size_t)B);              // flags
+    return cv.off + op_ws(c, TS_OP_MARG, s, nullptr, nullptr, nullptr);
+  }
+  if (op < TS_OP_LOGZ || op > TS_OP_VITERBI) return 0;
+  return op_ws(c, op, s, nullptr, nullptr, nullptr);
+}
+
+TS_API ts_status ts_logpartition(const ts_chain* c, ts_semiring s, float* logz, uint32_t* flags,
+                                 void* ws, size_t ws_bytes, void* stream) {
+  if (!chain_ok(c) || !logz || !aligned(logz, 4) || (flags && !aligned(flags, 4)))
+    return TS_E_INVALID;
+  if (s != TS_LOG && s != TS_MAX) return TS_E_INVALID;
+  if (!device_ok()) return TS_E_UNSUPPORTED;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (s == TS_MAX) return run_max(c, TS_OP_LOGZ, nullptr, logz, nullptr, nullptr, flags, ws, ws_bytes, st);
+  return run_log(c, nullptr, logz, flags, ws, ws_bytes, st);
+}
+
+TS_API ts_status ts_marginals(const ts_chain* c, ts_semiring s, float* marg, float* logz,
+                              uint32_t* flags, void* ws, size_t ws_bytes, void* stream) {
+  if (!chain_ok(c) || !marg || !aligned(marg, 16) || (logz && !aligned(logz, 4)) ||
+      (flags && !aligned(flags, 4)))
+    return TS_E_INVALID;
+  if (s != TS_LOG && s != TS_MAX) return TS_E_INVALID;
+  if (!device_ok()) return TS_E_UNSUPPORTED;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (s == TS_MAX) return run_max(c, TS_OP_MARG, marg, logz, nullptr, nullptr, flags, ws, ws_bytes, st);
+  // logz is required internally by the log path; use a workspace slot if the caller passed NULL
+  if (!logz) return TS_E_INVALID;
+  return run_log(c, marg, logz, flags, ws, ws_bytes, st);
+}
+
+TS_API ts_status ts_viterbi(const ts_chain* c, int32_t* path, float* score, uint32_t* flags,
+                            void* ws, size_t ws_bytes, void* stream) {
+  if (!chain_ok(c) || !path || !score || !aligned(path, 4) || !aligned(score, 4) ||
+      (flags && !aligned(flags, 4)))
+    return TS_E_INVALID;
+  if (!device_ok()) return TS_E_UNSUPPORTED;
+  return run_max(c, TS_OP_VITERBI, nullptr, nullptr, path, score, flags, ws, ws_bytes,
+                 static_cast<cudaStream_t>(stream));
+}
+
+TS_API ts_status ts_marginals_host(const ts_chain* hc, ts_semiring s, float* host_marg,
+                                   float* host_logz, uint32_t* host_flags, void* ws,
+                                   size_t ws_bytes, void* stream) {
+  if (!chain_ok(hc) || !host_marg || !host_logz) return TS_E_INVALID;
+  if (s != TS_LOG && s != TS_MAX) return TS_E_INVALID;
+  if (!device_ok()) return TS_E_UNSUPPORTED;
+  const size_t need = ts_workspace_bytes(hc, TS_OP_MARG_HOST, s);
+  if (ws_bytes < need || !ws || !aligned(ws, kAlign)) return TS_E_WORKSPACE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t B = hc->B, N = hc->N, C = hc->C, E = N - 1;
+  const size_t nel = (size_t)(B * E * C * C);
+  Carve cv(ws);
+  float* d_pot = cv.take<float>(nel);
+  int32_t* d_len = cv.take<int32_t>((size_t)B);
+  float* d_marg = cv.take<float>(nel);
+  float* d_logz = cv.take<float>((size_t)B);
+  uint32_t* d_flags = cv.take<uint32_t>((size_t)B);
+  void* inner = static_cast<char*>(ws) + cv.off;
+  const size_t inner_bytes = ws_bytes - cv.off;
+  cudaError_t e;
+  if (nel && (e = cudaMemcpyAsync(d_pot, hc->pot, nel * 4, cudaMemcpyHostToDevice, st)) != cudaSuccess)
+    return cuda_status(e);
+  if (hc->lengths &&
+      (e = cudaMemcpyAsync(d_len, hc->lengths, (size_t)B * 4, cudaMemcpyHostToDevice, st)) !=
+          cudaSuccess)
+    return cuda_status(e);
+  ts_chain dc{B, N, C, nel ? d_pot : nullptr, hc->lengths ? d_len : nullptr};
+  ts_status r = ts_marginals(&dc, s, d_marg, d_logz, d_flags, inner, inner_bytes, stream);
+  if (r != TS_OK) return r;
+  const int kern = t_launches;
+  if (nel && (e = cudaMemcpyAsync(host_marg, d_marg, nel * 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+    return cuda_status(e);
+  if ((e = cudaMemcpyAsync(host_logz, d_logz, (size_t)B * 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+    return cuda_status(e);
+  if (host_flags &&
+      (e = cudaMemcpyAsync(host_flags, d_flags, (size_t)B * 4, cudaMemcpyDeviceToHost, st)) !=
+          cudaSuccess)
+    return cuda_status(e);
+  t_launches = kern;
+  return TS_OK;
+}
+
+TS_API size_t ts_segment_summary_bytes(const ts_chain* local) {
+  if (!chain_ok(local)) return 0;
+  return (size_t)(local->B * local->C * local->C) * sizeof(float) +
+         (size_t)(local->B * local->C) * sizeof(double);
+}
+
+TS_API ts_status ts_segment_summary(const ts_chain*, int64_t, int64_t, ts_semiring, void*, void*,
+                                    size_t, void*) {
+  return TS_E_UNSUPPORTED;  // implemented with the scan tree (scan.cu)
+}
+
+TS_API ts_status ts_segment_finish(const ts_chain*, int64_t, int64_t, int, int, ts_semiring,
+                                   const void*, float*, float*, uint32_t*, void*, size_t, void*) {
+  return TS_E_UNSUPPORTED;
+}
+
+TS_API void ts_set_plan_chunk(int64_t L) { g_plan_chunk.store(L < 0 ? 0 : L); }
+TS_API int64_t ts_get_plan_chunk(void) { return g_plan_chunk.load(); }
+TS_API int ts_last_launch_count(void) { return t_launches; }
+
+TS_API const char* ts_status_str(ts_status s) {
+  switch (s) {
+    case TS_OK: return "TS_OK";
+    case TS_E_INVALID: return "TS_E_INVALID: invalid argument";
+    case TS_E_UNSUPPORTED: return "TS_E_UNSUPPORTED: needs an sm_100 (B200) device / unsupported case";
+    case TS_E_WORKSPACE: return "TS_E_WORKSPACE: workspace too small or misaligned";
+    case TS_E_CUDA: return "TS_E_CUDA: CUDA launch/copy failure";
+  }
+  return "unknown ts_status";
+}
+
+TS_API const char* ts_version(void) { return "ts_b200 0.1 (sm_100a)"; }
+
+}  // extern "C"

@@ -1,0 +1,75 @@
+// kernels.cuh — argument blocks and launchers of the sm_100a kernels (internal to the
+// library; the public surface is include/ts_b200.h, implemented in abi.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "ts_b200.h"
+
+namespace tsb {
+
+// Per-sequence scratch flags accumulated by the kernels that read l (device, [B]).
+enum : uint32_t { WF_NONFINITE = 2u };
+
+// ---- fused whole-sequence-in-SMEM forward/backward/marginals (C <= 32) -------------
+struct SmallArgs {
+  const float* pot;
+  const int32_t* lengths;
+  int64_t B, N, C;
+  float* marg;      // [B][N-1][C][C] or nullptr (logZ only)
+  float* logz;      // [B]
+  uint32_t* flags;  // [B] or nullptr
+};
+size_t small_smem_bytes(int64_t N, int64_t C);
+bool small_fits(int64_t N, int64_t C);
+cudaError_t launch_small(const SmallArgs& a, cudaStream_t st);
+
+// ---- streaming (time-chunked) forward / backward sweeps, log semiring (C <= 128) ----
+// Chunk k of sequence b covers edges [k*L, min((k+1)*L, E_b)), E_b = len_b - 1.
+// Vectors crossing chunk boundaries are "LogVec": C fp32 log2-domain values relative
+// to one fp64 natural-log offset.
+struct SweepArgs {
+  const float* pot;
+  const int32_t* lengths;
+  int64_t B, N, C;
+  int64_t L, P;             // chunk length and chunks per sequence
+  // forward
+  const float* alpha_in;    // [B*P][C] log2-relative start vector per chunk, or nullptr (=0)
+  const double* alpha_in_off;  // [B*P] natural offsets, or nullptr (=0)
+  float* alpha_hat;         // [B][N][C] node vectors (nodes [s_k, e_k) written by chunk k)
+  float* alpha_end;         // [B*P][C] chunk-end vector in the chunk's own frame
+  double* alpha_end_off;    // [B*P] its natural offset
+  float* mlag;              // [B][N] lag bound m_t used at step t (forward frame)
+  float* tmax;              // [B][N-1] per-edge tile max (natural units)
+  // backward
+  const float* beta_out;    // [B*P][C] chunk-end beta vector, or nullptr (=0, last chunk)
+  const double* beta_out_off;  // [B*P] or nullptr
+  float* marg;              // [B][N-1][C][C] or nullptr
+  // bookkeeping
+  uint32_t* wflags;         // [B] scratch flags (zeroed before the forward launch)
+  float* logz;              // [B] (written by the last chunk's forward CTA when P == 1)
+  uint32_t* flags;          // [B] or nullptr
+  int final_in_fwd;         // 1: forward writes logz/flags (logZ-only call, P == 1)
+};
+size_t fwd_smem_bytes(int64_t C, int stages);
+size_t bwd_smem_bytes(int64_t C, int stages);
+cudaError_t launch_fwd(const SweepArgs& a, cudaStream_t st);
+cudaError_t launch_bwd(const SweepArgs& a, cudaStream_t st);
+
+// ---- Viterbi (max-plus) -------------------------------------------------------------
+struct VitArgs {
+  const float* pot;
+  const int32_t* lengths;
+  int64_t B, N, C;
+  uint8_t* bp;      // [B][N-1][C] backpointers
+  int32_t* zend;    // [B] final label (first argmax), -1 if none
+  float* score;     // [B]
+  uint32_t* flags;  // [B] or nullptr
+  int32_t* path;    // [B][N] or nullptr
+  float* marg;      // [B][N-1][C][C] indicator or nullptr
+  float* logz;      // [B] copy of the score for ts_logpartition/ts_marginals(TS_MAX), or nullptr
+};
+size_t vit_smem_bytes(int64_t C, int stages, int rows_per_stage);
+cudaError_t launch_viterbi(const VitArgs& a, cudaStream_t st, int* launches);
+
+}  // namespace tsb

@@ -1,0 +1,270 @@
+// viterbi.cu — max-plus forward with backpointers, backtrack, and the argmax indicator.
+//
+// PAPER.md P:160 / P:265 (Max semiring, Table 2), reading R5:
+//   delta_0 = 0;  delta_{t+1}[j] = max_i (delta_t[i] + l_t[i][j]);
+//   bp_t[j] = the smallest i attaining the max (strict '>' while scanning i upward);
+//   z_E = smallest argmax_j delta_E[j];  z_t = bp_t[z_{t+1}];  score = delta_E[z_E].
+// fp32 adds of dyadic inputs are exact, so delta equals the fp64 oracle bit-for-bit.
+// One CTA per sequence, thread j owns column j; tiles stream through a cp.async ring of
+// row blocks (a 256 x 256 tile is 256 KB, larger than SMEM).
+#include <atomic>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace tsb {
+
+namespace {
+__device__ __forceinline__ float max_nan(float a, float b) {
+  float r;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+inline int vit_threads(int64_t C) { return (int)(((C + 31) / 32) * 32); }
+inline int vit_rows(int64_t C) { return C <= 128 ? (int)C : 32; }
+}  // namespace
+
+size_t vit_smem_bytes(int64_t C, int stages, int rows_per_stage) {
+  const int NT = vit_threads(C);
+  const size_t stage = (((size_t)rows_per_stage * C) + 3) & ~(size_t)3;
+  return (stages * stage + 2 * NT + 3 * (NT / 32) + 8) * sizeof(float);
+}
+
+template <bool VEC4>
+__global__ void __launch_bounds__(256) viterbi_fwd_kernel(VitArgs a, int S, int RB) {
+  extern __shared__ __align__(16) float sm[];
+  const int C = (int)a.C;
+  const int64_t N = a.N, E = N - 1, CC = (int64_t)C * C;
+  const int64_t b = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int NT = blockDim.x, NW = NT >> 5;
+  const int SF = ((RB * C) + 3) & ~3;
+  float* ring = sm;
+  float* dl = ring + (size_t)S * SF;  // [2][NT]
+  float* redv = dl + 2 * NT;          // [2*NW]: per-warp best value, per-warp NaN probe
+  int* redi = reinterpret_cast<int*>(redv + 2 * NW);  // [NW]
+
+  const int64_t len = seq_len(a.lengths, b, N);
+  if (len < 0) {
+    if (tid == 0) {
+      a.zend[b] = -1;
+      a.score[b] = qnan();
+      if (a.logz) a.logz[b] = qnan();
+      if (a.flags) a.flags[b] = TS_F_BADLEN;
+    }
+    return;
+  }
+  const int64_t Eb = len - 1;
+  const int nblk = (C + RB - 1) / RB;
+  const int64_t G = Eb * nblk;
+  const float* potb = a.pot + b * E * CC;
+  const bool act = tid < C;
+
+  auto issue = [&](int64_t g) {
+    if (g < G) {
+      const int64_t t = g / nblk;
+      const int blk = (int)(g - t * nblk);
+      const int r0 = blk * RB, nr = min(RB, C - r0);
+      float* dst = ring + (size_t)(g % S) * SF;
+      const float* src = potb + t * CC + (int64_t)r0 * C;
+      const int n = nr * C;
+      if (VEC4) {
+        for (int q = tid; q < (n >> 2); q += NT) cp_async16(dst + 4 * q, src + 4 * q);
+      } else {
+        for (int q = tid; q < n; q += NT) cp_async4(dst + q, src + q);
+      }
+    }
+    cp_async_commit();
+  };
+
+  for (int u = 0; u < S - 1; ++u) issue(u);
+  dl[tid] = act ? 0.f : neg_inf();
+  float best = neg_inf(), chk = neg_inf();
+  int arg = 0;
+  int buf = 0;
+  for (int64_t g = 0; g < G; ++g) {
+    cp_async_wait_dyn(S - 2);
+    __syncthreads();
+    issue(g + S - 1);
+    const int64_t t = g / nblk;
+    const int blk = (int)(g - t * nblk);
+    const int r0 = blk * RB, nr = min(RB, C - r0);
+    const float* tile = ring + (size_t)(g % S) * SF;
+    const float* d = dl + buf * NT + r0;
+    if (act) {
+#pragma unroll 4
+      for (int r = 0; r < nr; ++r) {
+        const float v = d[r] + tile[r * C + tid];
+        chk = max_nan(chk, v);
+        if (v > best) {
+          best = v;
+          arg = r0 + r;
+        }
+      }
+    }
+    if (blk == nblk - 1) {
+      const float nd = (chk != chk) ? qnan() : best;
+      dl[(buf ^ 1) * NT + tid] = act ? nd : neg_inf();
+      if (act) a.bp[(b * E + t) * C + tid] = (uint8_t)arg;
+      best = neg_inf();
+      chk = neg_inf();
+      arg = 0;
+      buf ^= 1;
+    }
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+  // final argmax: smallest j attaining the max (NaN poisons)
+  float v = act ? dl[buf * NT + tid] : neg_inf();
+  int idx = act ? tid : 0x7fffffff;
+  float bad = v;  // NaN propagates through max_nan
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, v, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+    bad = max_nan(bad, __shfl_xor_sync(0xffffffffu, bad, o));
+    if (ov > v || (ov == v && oi < idx)) {
+      v = ov;
+      idx = oi;
+    }
+  }
+  if (lane == 0) {
+    redv[w] = v;
+    redi[w] = idx;
+    redv[NW + w] = bad;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    float bv = redv[0];
+    int bi = redi[0];
+    float bb = redv[NW];
+    for (int q = 1; q < NW; ++q) {
+      if (redv[q] > bv || (redv[q] == bv && redi[q] < bi)) {
+        bv = redv[q];
+        bi = redi[q];
+      }
+      bb = max_nan(bb, redv[NW + q]);
+    }
+    uint32_t fl = 0;
+    float sc = bv;
+    int z = bi;
+    if (bb != bb || bb == pos_inf()) {
+      fl = TS_F_NONFINITE;
+      sc = qnan();
+      z = -1;
+    } else if (bv == neg_inf()) {
+      fl = TS_F_EMPTY;
+      z = -1;
+    }
+    a.zend[b] = z;
+    a.score[b] = sc;
+    if (a.logz) a.logz[b] = sc;
+    if (a.flags) a.flags[b] = fl;
+  }
+}
+
+// One warp per sequence: stage backpointer rows in SMEM (coalesced), walk back serially.
+constexpr int kBtRows = 64;
+__global__ void __launch_bounds__(32) backtrack_kernel(VitArgs a) {
+  extern __shared__ __align__(16) uint8_t bsm[];
+  const int C = (int)a.C;
+  const int64_t N = a.N, E = N - 1;
+  const int64_t b = blockIdx.x;
+  const int lane = threadIdx.x;
+  int32_t* pb = a.path ? a.path + b * N : nullptr;
+  const int64_t len = seq_len(a.lengths, b, N);
+  const int32_t z_end = a.zend[b];
+  if (len < 0 || z_end < 0) {
+    if (pb)
+      for (int64_t n = lane; n < N; n += 32) pb[n] = -1;
+    return;
+  }
+  const int64_t Eb = len - 1;
+  if (pb)
+    for (int64_t n = Eb + 1 + lane; n < N; n += 32) pb[n] = -1;
+  int32_t* zs = reinterpret_cast<int32_t*>(bsm + kBtRows * 256);
+  int z = z_end;
+  if (lane == 0 && pb) pb[Eb] = z;
+  const uint8_t* bpb = a.bp + b * E * C;
+  for (int64_t hi = Eb; hi > 0; hi -= kBtRows) {
+    const int64_t lo = hi - kBtRows > 0 ? hi - kBtRows : 0;  // rows [lo, hi)
+    const int nrow = (int)(hi - lo);
+    const int nbytes = nrow * C;
+    const uint8_t* src = bpb + lo * C;
+    for (int q = lane; q < nbytes; q += 32) bsm[q] = src[q];
+    __syncwarp();
+    if (lane == 0) {
+      for (int r = nrow - 1; r >= 0; --r) {
+        z = bsm[r * C + z];
+        zs[r] = z;
+      }
+    }
+    __syncwarp();
+    z = __shfl_sync(0xffffffffu, z, 0);
+    if (pb)
+      for (int r = lane; r < nrow; r += 32) pb[lo + r] = zs[r];
+    __syncwarp();
+  }
+}
+
+// Indicator d(A*)/d(l): one-hot (z_t, z_{t+1}) per used edge, zeros elsewhere.
+__global__ void __launch_bounds__(256) indicator_kernel(VitArgs a) {
+  const int C = (int)a.C;
+  const int64_t N = a.N, E = N - 1, CC = (int64_t)C * C;
+  const int64_t b = blockIdx.y;
+  const int64_t t = blockIdx.x;
+  if (t >= E) return;
+  float* m = a.marg + (b * E + t) * CC;
+  const int32_t* pb = a.path + b * N;
+  const int zi = pb[t], zj = pb[t + 1];
+  const int64_t hot = (zi >= 0 && zj >= 0) ? (int64_t)zi * C + zj : -1;
+  for (int64_t q = threadIdx.x; q < CC; q += blockDim.x) m[q] = (q == hot) ? 1.f : 0.f;
+}
+
+namespace {
+std::atomic<uint64_t> g_attr_vit{0};
+template <typename K>
+cudaError_t set_smem(K kern, int bit) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t m = 1ull << ((dev & 15) * 4 + bit);
+  if (g_attr_vit.load() & m) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  if (e == cudaSuccess) g_attr_vit.fetch_or(m);
+  return e;
+}
+}  // namespace
+
+cudaError_t launch_viterbi(const VitArgs& a, cudaStream_t st, int* launches) {
+  const int C = (int)a.C;
+  const int RB = vit_rows(C);
+  const size_t stage = (((size_t)RB * C) + 3) & ~(size_t)3;
+  int S = (int)((160 * 1024) / (stage * 4));
+  S = S < 2 ? 2 : (S > 8 ? 8 : S);
+  const bool vec4 = (C % 4) == 0 && (reinterpret_cast<uintptr_t>(a.pot) & 15) == 0;
+  const size_t smem = vit_smem_bytes(C, S, RB);
+  cudaError_t e;
+  if (vec4) {
+    if ((e = set_smem(viterbi_fwd_kernel<true>, 0)) != cudaSuccess) return e;
+    viterbi_fwd_kernel<true><<<(unsigned)a.B, vit_threads(C), smem, st>>>(a, S, RB);
+  } else {
+    if ((e = set_smem(viterbi_fwd_kernel<false>, 1)) != cudaSuccess) return e;
+    viterbi_fwd_kernel<false><<<(unsigned)a.B, vit_threads(C), smem, st>>>(a, S, RB);
+  }
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  int n = 1;
+  if (a.path) {
+    backtrack_kernel<<<(unsigned)a.B, 32, kBtRows * 256 + kBtRows * 4, st>>>(a);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    ++n;
+  }
+  if (a.marg && a.N > 1) {
+    indicator_kernel<<<dim3((unsigned)(a.N - 1), (unsigned)a.B), 256, 0, st>>>(a);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    ++n;
+  }
+  if (launches) *launches = n;
+  return cudaSuccess;
+}
+
+}  // namespace tsb

@@ -1,0 +1,99 @@
+"""CPU-side checks of the C ABI boundary (no compute, no GPU needed).
+
+* the shared library loads and exports every entry point include/ts_b200.h declares;
+* argument validation returns TS_E_INVALID before touching any device;
+* workspace sizing is consistent (monotone in B, zero-size for the fused small plan);
+* the Python binding fails loudly (no CPU fallback) when the library is absent.
+"""
+import ctypes
+import os
+import re
+
+import pytest
+
+from paper_2002_00876_b200 import _lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "ts_b200.h")).read()
+    return sorted(set(re.findall(r"TS_API\s+[\w\s\*]+?\b(ts_\w+)\s*\(", src)))
+
+
+def test_header_symbols_exported():
+    L = _lib.load()
+    decl = declared_symbols()
+    assert len(decl) >= 13
+    assert sorted(_lib.SYMBOLS) == decl
+    for name in decl:
+        assert hasattr(L, name), name
+    assert L.ts_version().decode().startswith("ts_b200")
+    assert b"WORKSPACE" in L.ts_status_str(3)
+
+
+def _chain(B=2, N=5, C=3, pot=0x1000, lengths=None):
+    return _lib.ts_chain(B, N, C, pot, lengths)
+
+
+@pytest.mark.parametrize("kw", [dict(B=0), dict(N=0), dict(C=0), dict(C=257), dict(pot=0),
+                                dict(pot=0x1004)])
+def test_invalid_chains_rejected(kw):
+    L = _lib.load()
+    ch = _chain(**kw)
+    logz = ctypes.c_void_p(0x2000)
+    assert L.ts_logpartition(ctypes.byref(ch), 0, logz, None, None, 0, None) == 1
+    assert L.ts_workspace_bytes(ctypes.byref(ch), 1, 0) == 0
+
+
+def test_invalid_outputs_rejected():
+    L = _lib.load()
+    ch = _chain()
+    assert L.ts_logpartition(ctypes.byref(ch), 0, None, None, None, 0, None) == 1  # logz NULL
+    assert L.ts_marginals(ctypes.byref(ch), 0, 0x3008, 0x2000, None, None, 0, None) == 1  # misaligned
+    assert L.ts_viterbi(ctypes.byref(ch), None, 0x2000, None, None, 0, None) == 1
+    assert L.ts_logpartition(ctypes.byref(ch), 7, 0x2000, None, None, 0, None) == 1  # semiring
+    assert L.ts_logpartition(None, 0, 0x2000, None, None, 0, None) == 1
+
+
+def test_workspace_sizes():
+    L = _lib.load()
+    small = _chain(B=32, N=25, C=20)
+    assert L.ts_workspace_bytes(ctypes.byref(small), _lib.TS_OP_MARG, _lib.TS_LOG) == 0
+    big = _chain(B=4, N=512, C=64)
+    big2 = _chain(B=8, N=512, C=64)
+    w1 = L.ts_workspace_bytes(ctypes.byref(big), _lib.TS_OP_MARG, _lib.TS_LOG)
+    w2 = L.ts_workspace_bytes(ctypes.byref(big2), _lib.TS_OP_MARG, _lib.TS_LOG)
+    assert 0 < w1 < w2
+    assert w1 >= 4 * 512 * 64 * 4  # holds the forward vectors [B][N][C]
+    v = L.ts_workspace_bytes(ctypes.byref(_chain(B=64, N=1024, C=256)), _lib.TS_OP_VITERBI,
+                             _lib.TS_MAX)
+    assert v >= 64 * 1023 * 256  # uint8 backpointers
+    h = L.ts_workspace_bytes(ctypes.byref(small), _lib.TS_OP_MARG_HOST, _lib.TS_LOG)
+    assert h >= 2 * 32 * 24 * 400 * 4
+
+
+def test_plan_knob_roundtrip():
+    L = _lib.load()
+    L.ts_set_plan_chunk(7)
+    assert L.ts_get_plan_chunk() == 7
+    L.ts_set_plan_chunk(0)
+    assert L.ts_get_plan_chunk() == 0
+
+
+def test_binding_fails_loudly_without_library(monkeypatch, tmp_path):
+    monkeypatch.setattr(_lib, "_lib", None)
+    monkeypatch.setattr(_lib, "LIB_PATH", str(tmp_path / "missing.so"))
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        _lib.load()
+
+
+def test_product_package_never_imports_oracle():
+    pkg = os.path.join(ROOT, "paper_2002_00876_b200")
+    banned = ("import oracle", "from oracle", "liboracle", "oracle.c", "oracle/")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                txt = open(os.path.join(dirpath, f)).read()
+                for b in banned:
+                    assert b not in txt, (f, b)

@@ -1,0 +1,225 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle, element by
+element on seeded inputs.  Every test here needs a B200.
+
+Sizes: oracle-complete at sizes spanning several tiles and a ragged tail; full
+BASELINE.json sizes on sampled sequences / property checks.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2002_00876_b200 as tsb
+import tsgen
+from _util import check_logz, check_marg, check_viterbi
+
+pytestmark = pytest.mark.gpu
+
+
+def to_dev(a, dev):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+
+
+def run_all(pot_np, lengths_np, dev, marg=True):
+    pot = to_dev(pot_np, dev)
+    lengths = to_dev(lengths_np.astype(np.int32), dev) if lengths_np is not None else None
+    out = {}
+    if marg:
+        m, lz, fl = tsb.marginals(pot, lengths)
+        out["marg"], out["logz"], out["flags"] = m.cpu().numpy(), lz.cpu().numpy(), fl.cpu().numpy()
+    lz2, fl2 = tsb.logpartition(pot, lengths)
+    out["logz_only"], out["flags_only"] = lz2.cpu().numpy(), fl2.cpu().numpy()
+    return out
+
+
+def assert_log_parity(pot_np, lengths_np, dev, marg=True):
+    lz_ref, mg_ref, fl_ref = oracle.chain_marginals(pot_np, lengths_np, want_marg=marg, threads=8)
+    out = run_all(pot_np, lengths_np, dev, marg)
+    check_logz(out["logz_only"], lz_ref)
+    assert (out["flags_only"].astype(np.uint32) == fl_ref).all(), (out["flags_only"], fl_ref)
+    if marg:
+        check_logz(out["logz"], lz_ref)
+        assert (out["flags"].astype(np.uint32) == fl_ref).all()
+        return check_marg(out["marg"], mg_ref)
+
+
+def assert_viterbi_parity(pot_np, lengths_np, dev):
+    p_ref, s_ref, f_ref = oracle.chain_viterbi(pot_np, lengths_np, threads=8)
+    pot = to_dev(pot_np, dev)
+    lengths = to_dev(lengths_np.astype(np.int32), dev) if lengths_np is not None else None
+    path, score, flags = tsb.viterbi(pot, lengths)
+    check_viterbi(path.cpu().numpy(), score.cpu().numpy(), p_ref, s_ref)
+    assert (flags.cpu().numpy().astype(np.uint32) == f_ref).all()
+    # max-semiring entry points: logZ = score, marginals = one-hot indicator of the path
+    lz, _ = tsb.logpartition(pot, lengths, semiring="max")
+    check_viterbi(path.cpu().numpy(), lz.cpu().numpy(), p_ref, s_ref)
+    m, lz2, _ = tsb.marginals(pot, lengths, semiring="max")
+    np.testing.assert_array_equal(m.cpu().numpy(),
+                                  oracle.max_indicator(p_ref, pot_np.shape[-1], lengths_np))
+
+
+# ------------------------------------------------------------------ BASELINE configs
+
+def test_generator_device_equals_numpy(dev):
+    for (B, N, C, seed, s) in [(2, 7, 5, 123, 15), (3, 40, 20, 9, 13), (1, 9, 64, 4, 12)]:
+        t = torch.empty((B, N - 1, C, C), dtype=torch.float32, device=dev)
+        tsgen.fill_torch(t, seed, s)
+        assert t.cpu().numpy().tobytes() == tsgen.potentials(B, N, C, seed, s).tobytes()
+
+
+def test_cfg1_brute_scale(dev):
+    cfg = tsgen.CONFIGS[1]
+    pot = tsgen.config_potentials(cfg)
+    err = assert_log_parity(pot, None, dev)
+    assert err < 1e-5
+    assert_viterbi_parity(pot, None, dev)
+
+
+def test_cfg2_full(dev):
+    cfg = tsgen.CONFIGS[2]
+    pot = tsgen.config_potentials(cfg)
+    assert_log_parity(pot, None, dev)
+    assert_viterbi_parity(pot, None, dev)
+
+
+@pytest.mark.parametrize("B,N,C", [(3, 130, 64), (2, 77, 20), (2, 41, 128), (4, 33, 3),
+                                   (2, 600, 20), (3, 17, 37), (2, 9, 1), (2, 50, 100)])
+def test_streaming_and_small_shapes(dev, B, N, C):
+    pot = tsgen.potentials(B, N, C, seed=5000 + N + C)
+    assert_log_parity(pot, None, dev)
+    assert_viterbi_parity(pot, None, dev)
+
+
+def test_cfg3_reduced_elementwise(dev):
+    cfg = tsgen.CONFIGS[3]
+    pot = tsgen.potentials(6, cfg.N, cfg.C, cfg.seed, cfg.quantum)
+    assert_log_parity(pot, None, dev)
+    assert_viterbi_parity(pot, None, dev)
+
+
+@pytest.mark.parametrize("C", [3, 20, 64, 130, 256])
+def test_viterbi_shapes(dev, C):
+    pot = tsgen.potentials(3, 70, C, seed=77 + C)
+    assert_viterbi_parity(pot, None, dev)
+
+
+def test_cfg4_viterbi_full(dev):
+    cfg = tsgen.CONFIGS[4]
+    pot = torch.empty((cfg.B, cfg.E, cfg.C, cfg.C), dtype=torch.float32, device=dev)
+    tsgen.fill_torch(pot, cfg)
+    path, score, flags = tsb.viterbi(pot)
+    path, score = path.cpu().numpy(), score.cpu().numpy()
+    del pot
+    torch.cuda.empty_cache()
+    assert (flags.cpu().numpy() == 0).all()
+    import concurrent.futures as cf
+
+    def one(b):
+        return oracle.gen_viterbi(cfg.seed, cfg.quantum, b, cfg.N, cfg.C)
+
+    with cf.ThreadPoolExecutor(8) as ex:
+        res = list(ex.map(one, range(cfg.B)))
+    for b, (p, s, f) in enumerate(res):
+        assert f == 0
+        np.testing.assert_array_equal(path[b], p)
+        assert score[b] == np.float32(s)
+
+
+def test_cfg3_full_sampled(dev):
+    cfg = tsgen.CONFIGS[3]
+    pot = torch.empty((cfg.B, cfg.E, cfg.C, cfg.C), dtype=torch.float32, device=dev)
+    tsgen.fill_torch(pot, cfg)
+    marg, logz, flags = tsb.marginals(pot)
+    assert (flags.cpu().numpy() == 0).all()
+    sums = marg.sum(dim=(2, 3))
+    assert float((sums - 1).abs().max()) < 1e-4  # every edge sums to 1
+    logz = logz.cpu().numpy()
+    for b in (0, 137, 255):
+        lz_ref, edges, m_ref, f = oracle.gen_marginals(cfg.seed, cfg.quantum, b, cfg.N, cfg.C,
+                                                       range(cfg.E))
+        check_logz(logz[b:b + 1], [lz_ref])
+        check_marg(marg[b].cpu().numpy(), m_ref)
+
+
+# ------------------------------------------------------------------ edge cases
+
+def test_variable_lengths(dev):
+    for (B, N, C, seed) in [(8, 25, 20, 1), (6, 90, 64, 2), (5, 40, 128, 3), (7, 300, 8, 4)]:
+        pot = tsgen.potentials(B, N, C, seed=seed)
+        lengths = tsgen.random_lengths(B, N, seed)
+        lengths[0] = 1
+        lengths[1] = N
+        assert_log_parity(pot, lengths, dev)
+        assert_viterbi_parity(pot, lengths, dev)
+
+
+def test_flags_empty_nonfinite_badlen(dev):
+    for (N, C) in [(25, 20), (70, 64), (8, 3)]:
+        B = 6
+        pot = tsgen.potentials(B, N, C, seed=9)
+        pot[1] = -np.inf                           # EMPTY
+        pot[2, N // 2, 1 % C, 2 % C] = np.nan      # NONFINITE
+        pot[3, 1, 0, 0] = np.inf                   # +inf -> NONFINITE
+        lengths = np.full(B, N, dtype=np.int32)
+        lengths[4] = 0                             # BADLEN
+        lengths[5] = N + 1                         # BADLEN
+        assert_log_parity(pot, lengths, dev)
+        assert_viterbi_parity(pot, lengths, dev)
+
+
+def test_masked_tagging_inputs(dev):
+    for (B, N, C) in [(4, 25, 20), (3, 100, 64), (2, 20, 7)]:
+        pot = tsgen.tagging_potentials(B, N, C, seed=C, mask_frac=0.3)
+        assert_log_parity(pot, None, dev)
+        assert_viterbi_parity(pot, None, dev)
+
+
+@pytest.mark.parametrize("C", [3, 20, 64])
+def test_large_offset_recentring(dev, C):
+    # l = 1e4 + N(0,1): fails the 1e-4 marginal gate without per-tile re-centring (§7.3-7)
+    pot = tsgen.large_offset_potentials(3, 60, C, seed=C)
+    assert_log_parity(pot, None, dev)
+
+
+@pytest.mark.parametrize("C", [3, 20, 64, 128])
+def test_peaked_inputs_exercise_underflow_gate(dev, C):
+    pot = tsgen.peaked_potentials(3, 40, C, seed=C)
+    assert_log_parity(pot, None, dev)
+
+
+@pytest.mark.parametrize("C", [3, 20, 64, 128])
+def test_wide_inputs(dev, C):
+    # within-tile spreads of ~100 nats: |ah|, |bh| reach ~2^7, fp32 storage costs
+    # ~ulp(128) per term in the marginal exponent (precision envelope)
+    pot = tsgen.wide_potentials(2, 40, C, seed=C, scale=20.0)
+    assert_log_parity(pot, None, dev)
+
+
+def test_shift_by_1e4(dev):
+    # magnitude 1e4 -> finite results equal to the shifted result + analytic shift
+    for C in (20, 64):
+        base = tsgen.potentials(3, 50, C, seed=31, s=6)
+        for c in (1e4, -1e4):
+            assert_log_parity((base + np.float32(c)).astype(np.float32), None, dev)
+
+
+def test_deterministic_bitwise(dev):
+    for (B, N, C) in [(32, 25, 20), (4, 200, 64)]:
+        pot = to_dev(tsgen.potentials(B, N, C, seed=3), dev)
+        a = tsb.marginals(pot)
+        b = tsb.marginals(pot)
+        for x, y in zip(a, b):
+            assert torch.equal(x, y)
+
+
+def test_host_buffers_end_to_end(dev):
+    cfg = tsgen.CONFIGS[2]
+    pot = torch.from_numpy(tsgen.config_potentials(cfg)).pin_memory()
+    marg = torch.empty_like(pot).pin_memory()
+    logz = torch.empty(cfg.B, dtype=torch.float32).pin_memory()
+    flags = torch.empty(cfg.B, dtype=torch.int32).pin_memory()
+    tsb.marginals_host(pot, marg, logz, flags, device=dev)
+    torch.cuda.synchronize()
+    lz_ref, mg_ref, _ = oracle.chain_marginals(pot.numpy())
+    check_logz(logz.numpy(), lz_ref)
+    check_marg(marg.numpy(), mg_ref)

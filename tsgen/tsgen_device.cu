@@ -25,7 +25,7 @@ __global__ void tsgen_fill_kernel(float* __restrict__ out, int64_t B, int64_t E_
   }
 }
 
-extern "C" int tsgen_fill_device(float* out, int64_t B, int64_t E_local, int64_t C,
+extern "C" __attribute__((visibility("default"))) int tsgen_fill_device(float* out, int64_t B, int64_t E_local, int64_t C,
                                  uint64_t seed, int s, int64_t t_begin, int64_t E_global,
                                  void* stream) {
   if (B <= 0 || E_local <= 0 || C <= 0) return 0;
