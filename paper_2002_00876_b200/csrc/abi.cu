@@ -62,18 +62,62 @@ bool device_ok() {
   return v == 1;
 }
 
-enum class Plan { Small, Stream, Unsupported };
+enum class PlanKind { Small, Stream, Unsupported };
+struct Plan {
+  PlanKind kind;
+  int64_t L, P, Ppad;
+  int H;
+};
 
+// Plan selection: the fused small kernel for short chains with C <= 32;
+// otherwise the streaming sweeps, time-chunked with the scan tree when the batch alone
+// cannot fill the GPU (or when the debug knob asks for a chunk length).
 Plan log_plan(const ts_chain* c) {
-  const int64_t L = g_plan_chunk.load();
+  const int64_t knob = g_plan_chunk.load();
   const int64_t E = c->N - 1;
-  const bool serial_ok = (L == 0 || L >= E);
-  if (serial_ok && small_fits(c->N, c->C)) return Plan::Small;
-  if (c->C <= 128) return Plan::Stream;
-  return Plan::Unsupported;
+  Plan p{PlanKind::Stream, E > 0 ? E : 1, 1, 1, 0};
+  int64_t P = 1;
+  if (knob == 0) {
+    if (small_fits(c->N, c->C)) {
+      p.kind = PlanKind::Small;
+      return p;
+    }
+    int sms = 148;
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess)
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (c->B < sms && E >= 64) {
+      P = (sms + c->B - 1) / c->B;
+      const int64_t cap = (E + 31) / 32;  // chunks of at least 32 edges
+      if (P > cap) P = cap;
+    }
+  } else if (knob < E) {
+    P = (E + knob - 1) / knob;
+  } else if (small_fits(c->N, c->C)) {
+    p.kind = PlanKind::Small;
+    return p;
+  }
+  if (c->C > 128) {
+    p.kind = PlanKind::Unsupported;
+    return p;
+  }
+  if (P > 1) {
+    p.P = P;
+    p.L = (knob > 0 && knob < E) ? knob : (E + P - 1) / P;
+    p.P = (E + p.L - 1) / p.L;
+    int64_t pp = 1;
+    int h = 0;
+    while (pp < p.P) {
+      pp <<= 1;
+      ++h;
+    }
+    p.Ppad = pp;
+    p.H = h;
+  }
+  return p;
 }
 
-// Workspace layout of the streaming log path (P = 1).
+// Workspace layout of the streaming log path.
 struct StreamWs {
   float* alpha_hat = nullptr;
   float* mlag = nullptr;
@@ -82,19 +126,53 @@ struct StreamWs {
   double* alpha_end_off = nullptr;
   uint32_t* wflags = nullptr;
 };
-size_t stream_ws(const ts_chain* c, bool marg, void* ws, StreamWs* out) {
+struct ScanWs {
+  float* mat = nullptr;
+  double* off = nullptr;
+  uint8_t* ident = nullptr;
+  uint32_t* cflag = nullptr;
+  float* valpha = nullptr;
+  double* oalpha = nullptr;
+  float* vbeta = nullptr;
+  double* obeta = nullptr;
+  float* leaf_alpha = nullptr;
+  double* leaf_alpha_off = nullptr;
+  float* leaf_beta = nullptr;
+  double* leaf_beta_off = nullptr;
+};
+size_t stream_ws(const ts_chain* c, const Plan& pl, bool marg, void* ws, StreamWs* out,
+                 ScanWs* sout) {
   Carve cv(ws);
   StreamWs w;
-  const int64_t B = c->B, N = c->N, C = c->C, E = N - 1;
+  ScanWs s;
+  const int64_t B = c->B, N = c->N, C = c->C, E = N - 1, P = pl.P;
   if (marg) {
     w.alpha_hat = cv.take<float>((size_t)(B * N * C));
     w.mlag = cv.take<float>((size_t)(B * N));
     w.tmax = cv.take<float>((size_t)(B * (E > 0 ? E : 1)));
   }
-  w.alpha_end = cv.take<float>((size_t)(B * C));
-  w.alpha_end_off = cv.take<double>((size_t)B);
+  w.alpha_end = cv.take<float>((size_t)(B * P * C));
+  w.alpha_end_off = cv.take<double>((size_t)(B * P));
   w.wflags = cv.take<uint32_t>((size_t)B);
+  if (P > 1) {
+    const int64_t nodes = 2 * pl.Ppad - 1;
+    s.mat = cv.take<float>((size_t)(B * nodes * C * C));
+    s.off = cv.take<double>((size_t)(B * nodes * C));
+    s.ident = cv.take<uint8_t>((size_t)(B * nodes));
+    s.cflag = cv.take<uint32_t>((size_t)(B * pl.Ppad));
+    if (marg) {
+      s.valpha = cv.take<float>((size_t)(B * nodes * C));
+      s.oalpha = cv.take<double>((size_t)(B * nodes));
+      s.vbeta = cv.take<float>((size_t)(B * nodes * C));
+      s.obeta = cv.take<double>((size_t)(B * nodes));
+      s.leaf_alpha = cv.take<float>((size_t)(B * P * C));
+      s.leaf_alpha_off = cv.take<double>((size_t)(B * P));
+      s.leaf_beta = cv.take<float>((size_t)(B * P * C));
+      s.leaf_beta_off = cv.take<double>((size_t)(B * P));
+    }
+  }
   if (out) *out = w;
+  if (sout) *sout = s;
   return cv.off;
 }
 
@@ -127,8 +205,8 @@ size_t op_ws(const ts_chain* c, int op, ts_semiring s, void* ws, StreamWs* sw, V
   }
   if (op == TS_OP_VITERBI) return vit_ws(c, false, false, ws, vw);
   const Plan p = log_plan(c);
-  if (p == Plan::Small) return 0;
-  return stream_ws(c, op == TS_OP_MARG, ws, sw);
+  if (p.kind != PlanKind::Stream) return 0;
+  return stream_ws(c, p, op == TS_OP_MARG, ws, sw, nullptr);
 }
 
 ts_status cuda_status(cudaError_t e) {
@@ -140,24 +218,67 @@ ts_status cuda_status(cudaError_t e) {
 ts_status run_log(const ts_chain* c, float* marg, float* logz, uint32_t* flags, void* ws,
                   size_t ws_bytes, cudaStream_t st) {
   const Plan p = log_plan(c);
-  if (p == Plan::Unsupported) return TS_E_UNSUPPORTED;
-  if (p == Plan::Small) {
+  if (p.kind == PlanKind::Unsupported) return TS_E_UNSUPPORTED;
+  if (p.kind == PlanKind::Small) {
     SmallArgs a{c->pot, c->lengths, c->B, c->N, c->C, marg, logz, flags};
     ts_status r = cuda_status(launch_small(a, st));
     if (r == TS_OK) t_launches = 1;
     return r;
   }
   StreamWs w;
-  const size_t need = stream_ws(c, marg != nullptr, ws, &w);
+  ScanWs sw;
+  const size_t need = stream_ws(c, p, marg != nullptr, ws, &w, &sw);
   if (ws_bytes < need || (need && (!ws || !aligned(ws, kAlign)))) return TS_E_WORKSPACE;
+  cudaError_t e = cudaMemsetAsync(w.wflags, 0, sizeof(uint32_t) * (size_t)c->B, st);
+  if (e != cudaSuccess) return cuda_status(e);
+  int n = 0;
+  ScanArgs sa{};
+  if (p.P > 1) {
+    sa.pot = c->pot;
+    sa.lengths = c->lengths;
+    sa.B = c->B;
+    sa.N = c->N;
+    sa.C = c->C;
+    sa.L = p.L;
+    sa.P = p.P;
+    sa.Ppad = p.Ppad;
+    sa.nodes = 2 * p.Ppad - 1;
+    sa.H = p.H;
+    sa.mat = sw.mat;
+    sa.off = sw.off;
+    sa.ident = sw.ident;
+    sa.cflag = sw.cflag;
+    sa.valpha = sw.valpha;
+    sa.oalpha = sw.oalpha;
+    sa.vbeta = sw.vbeta;
+    sa.obeta = sw.obeta;
+    sa.leaf_alpha = sw.leaf_alpha;
+    sa.leaf_alpha_off = sw.leaf_alpha_off;
+    sa.leaf_beta = sw.leaf_beta;
+    sa.leaf_beta_off = sw.leaf_beta_off;
+    sa.wflags = w.wflags;
+    sa.logz = logz;
+    sa.flags = flags;
+    if ((e = launch_scan_up(sa, st, &n)) != cudaSuccess) return cuda_status(e);
+    if (!marg) {  // logZ from the root of the Fig. 4 tree
+      if ((e = launch_scan_logz(sa, st)) != cudaSuccess) return cuda_status(e);
+      t_launches = n + 1;
+      return TS_OK;
+    }
+    if ((e = launch_scan_down(sa, st, &n)) != cudaSuccess) return cuda_status(e);
+  }
   SweepArgs a{};
   a.pot = c->pot;
   a.lengths = c->lengths;
   a.B = c->B;
   a.N = c->N;
   a.C = c->C;
-  a.L = (c->N > 1) ? c->N - 1 : 1;
-  a.P = 1;
+  a.L = p.L;
+  a.P = p.P;
+  a.alpha_in = sw.leaf_alpha;
+  a.alpha_in_off = sw.leaf_alpha_off;
+  a.beta_out = sw.leaf_beta;
+  a.beta_out_off = sw.leaf_beta_off;
   a.alpha_hat = w.alpha_hat;
   a.alpha_end = w.alpha_end;
   a.alpha_end_off = w.alpha_end_off;
@@ -168,11 +289,9 @@ ts_status run_log(const ts_chain* c, float* marg, float* logz, uint32_t* flags, 
   a.logz = logz;
   a.flags = flags;
   a.final_in_fwd = marg ? 0 : 1;
-  cudaError_t e = cudaMemsetAsync(w.wflags, 0, sizeof(uint32_t) * (size_t)c->B, st);
-  if (e != cudaSuccess) return cuda_status(e);
   e = launch_fwd(a, st);
   if (e != cudaSuccess) return cuda_status(e);
-  int n = 1;
+  ++n;
   if (marg) {
     e = launch_bwd(a, st);
     if (e != cudaSuccess) return cuda_status(e);

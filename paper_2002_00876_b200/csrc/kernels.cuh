@@ -56,6 +56,38 @@ size_t bwd_smem_bytes(int64_t C, int stages);
 cudaError_t launch_fwd(const SweepArgs& a, cudaStream_t st);
 cudaError_t launch_bwd(const SweepArgs& a, cudaStream_t st);
 
+// ---- time-chunked scan (scan.cu): leaf summaries, up-sweep tree, down-sweep ---------
+// Tree of one sequence: levels 0..H, level l holds Ppad >> l nodes (Ppad = 2^H >= P),
+// `nodes` = 2*Ppad - 1 node slots per sequence.  LogMat node: mat [C][C] log2 values +
+// off [C] fp64 natural row offsets; ident = 1 marks the identity I (padding).
+struct ScanArgs {
+  const float* pot;
+  const int32_t* lengths;
+  int64_t B, N, C;
+  int64_t L, P, Ppad, nodes;
+  int H;
+  float* mat;
+  double* off;
+  uint8_t* ident;
+  uint32_t* cflag;  // [B][Ppad] leaf chunks needing the exact log-space recomputation
+  float* valpha;    // [B][nodes][C] alpha_in vector of every node
+  double* oalpha;
+  float* vbeta;     // [B][nodes][C] beta_out vector of every node
+  double* obeta;
+  float* leaf_alpha;  // [B][P][C] leaf copies read by the leaf sweeps
+  double* leaf_alpha_off;
+  float* leaf_beta;
+  double* leaf_beta_off;
+  uint32_t* wflags;
+  float* logz;
+  uint32_t* flags;
+};
+__host__ __device__ int64_t level_off(int l, int64_t Ppad);
+size_t scan_mat_smem(int64_t C);
+cudaError_t launch_scan_up(const ScanArgs& a, cudaStream_t st, int* launches);
+cudaError_t launch_scan_down(const ScanArgs& a, cudaStream_t st, int* launches);
+cudaError_t launch_scan_logz(const ScanArgs& a, cudaStream_t st);
+
 // ---- Viterbi (max-plus) -------------------------------------------------------------
 struct VitArgs {
   const float* pot;
