@@ -123,16 +123,19 @@ TS_API ts_status ts_marginals_host(const ts_chain *host_chain, ts_semiring s, fl
  * [edge_begin, edge_begin + local->N - 1) in local->pot (local->N = local edge count + 1)
  * for every sequence of the batch (local->lengths must be NULL: full-length chains).
  * Step 1: ts_segment_summary writes this segment's C x C transfer matrix per sequence
- *         (the semiring product of its edges) into `summary`, laid out as
- *         ts_segment_summary_bytes(local) bytes: [B][C][C] fp32 log2-domain values
- *         relative to a per-sequence fp64 scale, followed by [B] fp64 scales.
+ *         (the semiring product of its edges) into `summary` (16-byte aligned),
+ *         laid out as ts_segment_summary_bytes(local) bytes: [B][C][C] fp32 log2-domain
+ *         values relative to per-row fp64 natural-log offsets, followed by [B][C] fp64
+ *         offsets.  The workspace (size: ts_workspace_bytes(local, TS_OP_SEGMENT, s)) holds
+ *         the local scan tree and MUST be passed unchanged to ts_segment_finish.
  * Step 2: the caller all-gathers the summaries of all `world` segments, in rank order,
  *         into all_summaries ([world] x ts_segment_summary_bytes) — e.g. NCCL
  *         all_gather_into_tensor over NVLink.
  * Step 3: ts_segment_finish combines them (every rank computes the same prefix/suffix
  *         products in the same order, so logZ is bit-identical across ranks) and runs the
  *         local forward/backward sweeps: logz [B] (global A), marg (local edges) or NULL.
- * TS_MAX is supported for the summary/logz (score) only in this round. */
+ * Only TS_LOG is implemented (TS_MAX returns TS_E_UNSUPPORTED); C <= 128; lengths NULL.
+ * logz/flags are global (identical on every rank); marg covers the local edges. */
 TS_API size_t ts_segment_summary_bytes(const ts_chain *local);
 TS_API ts_status ts_segment_summary(const ts_chain *local, int64_t edge_begin, int64_t n_global,
                                     ts_semiring s, void *summary, void *ws, size_t ws_bytes,

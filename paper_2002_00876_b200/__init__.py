@@ -21,7 +21,8 @@ from . import _lib
 from ._lib import TS_F_BADLEN, TS_F_EMPTY, TS_F_NONFINITE, TsError  # noqa: F401
 
 __all__ = ["logpartition", "marginals", "viterbi", "marginals_host", "set_plan_chunk",
-           "get_plan_chunk", "last_launch_count", "workspace_bytes", "Workspace", "TsError"]
+           "get_plan_chunk", "last_launch_count", "workspace_bytes", "Workspace", "TsError",
+           "Segment"]
 
 _SEMI = {"log": _lib.TS_LOG, "max": _lib.TS_MAX}
 
@@ -153,6 +154,54 @@ def marginals_host(pot_host: torch.Tensor, marg_host: torch.Tensor, logz_host: t
                                    logz_host.data_ptr(),
                                    flags_host.data_ptr() if flags_host is not None else None, wp,
                                    need, _stream(device)), "ts_marginals_host")
+
+
+class Segment:
+    """One rank's contiguous time segment of a long chain (time sharding).
+
+    Holds the device workspace (the local scan tree) between `summary()` and `finish()`.
+    `local_pot` [B, E_local, C, C] holds global edges [edge_begin, edge_begin + E_local) of
+    chains with `n_global` positions (full length; no per-sequence lengths).
+    """
+
+    def __init__(self, local_pot: torch.Tensor, edge_begin: int, n_global: int):
+        self.pot = local_pot
+        self.edge_begin = int(edge_begin)
+        self.n_global = int(n_global)
+        self.ch = _chain(local_pot, None)
+        L = _lib.load()
+        self.nbytes = int(L.ts_segment_summary_bytes(ctypes.byref(self.ch)))
+        self.ws_bytes = int(L.ts_workspace_bytes(ctypes.byref(self.ch), _lib.TS_OP_SEGMENT,
+                                                 _lib.TS_LOG))
+        self.ws = Workspace(local_pot.device)
+        self.wptr = self.ws.ptr(self.ws_bytes)
+
+    def summary(self) -> torch.Tensor:
+        """This segment's C x C transfer matrices (the local semiring product) as
+        float32 words [B*C*C + 2*B*C] (fp64 row offsets packed after the matrices)."""
+        L = _lib.load()
+        out = torch.empty(self.nbytes // 4, dtype=torch.float32, device=self.pot.device)
+        _lib.check(L.ts_segment_summary(ctypes.byref(self.ch), self.edge_begin, self.n_global,
+                                        _lib.TS_LOG, out.data_ptr(), self.wptr, self.ws_bytes,
+                                        _stream(self.pot.device)), "ts_segment_summary")
+        return out
+
+    def finish(self, all_summaries: torch.Tensor, rank: int, world: int, want_marg: bool = True):
+        """Combine the gathered summaries [world, nbytes/4] (rank order) -> (marg|None, logz, flags)."""
+        L = _lib.load()
+        B = self.pot.shape[0]
+        dev = self.pot.device
+        all_summaries = all_summaries.contiguous()
+        marg = torch.empty_like(self.pot) if want_marg else None
+        logz = torch.empty(B, dtype=torch.float32, device=dev)
+        flags = torch.empty(B, dtype=torch.int32, device=dev)
+        _lib.check(L.ts_segment_finish(ctypes.byref(self.ch), self.edge_begin, self.n_global,
+                                       int(rank), int(world), _lib.TS_LOG,
+                                       all_summaries.data_ptr(),
+                                       marg.data_ptr() if want_marg else None, logz.data_ptr(),
+                                       flags.data_ptr(), self.wptr, self.ws_bytes, _stream(dev)),
+                   "ts_segment_finish")
+        return marg, logz, flags
 
 
 def set_plan_chunk(L: int) -> None:

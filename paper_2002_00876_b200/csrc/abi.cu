@@ -141,7 +141,7 @@ struct ScanWs {
   double* leaf_beta_off = nullptr;
 };
 size_t stream_ws(const ts_chain* c, const Plan& pl, bool marg, void* ws, StreamWs* out,
-                 ScanWs* sout) {
+                 ScanWs* sout, bool force_tree = false) {
   Carve cv(ws);
   StreamWs w;
   ScanWs s;
@@ -154,7 +154,7 @@ size_t stream_ws(const ts_chain* c, const Plan& pl, bool marg, void* ws, StreamW
   w.alpha_end = cv.take<float>((size_t)(B * P * C));
   w.alpha_end_off = cv.take<double>((size_t)(B * P));
   w.wflags = cv.take<uint32_t>((size_t)B);
-  if (P > 1) {
+  if (P > 1 || force_tree) {
     const int64_t nodes = 2 * pl.Ppad - 1;
     s.mat = cv.take<float>((size_t)(B * nodes * C * C));
     s.off = cv.take<double>((size_t)(B * nodes * C));
@@ -265,7 +265,7 @@ ts_status run_log(const ts_chain* c, float* marg, float* logz, uint32_t* flags, 
       t_launches = n + 1;
       return TS_OK;
     }
-    if ((e = launch_scan_down(sa, st, &n)) != cudaSuccess) return cuda_status(e);
+    if ((e = launch_scan_down(sa, st, &n, true)) != cudaSuccess) return cuda_status(e);
   }
   SweepArgs a{};
   a.pot = c->pot;
@@ -326,6 +326,60 @@ ts_status run_max(const ts_chain* c, int op, float* marg, float* logz, int32_t* 
   return r;
 }
 
+// Plan of a time-sharded segment: always the scan tree (P >= 1), chunked like log_plan.
+Plan seg_plan(const ts_chain* c) {
+  Plan p = log_plan(c);
+  const int64_t E = c->N - 1;
+  if (p.kind == PlanKind::Small) {  // segments always run through the tree
+    p.kind = PlanKind::Stream;
+    p.P = 1;
+    p.L = E > 0 ? E : 1;
+  }
+  if (p.P <= 1) {
+    p.P = 1;
+    p.Ppad = 1;
+    p.H = 0;
+    p.L = E > 0 ? E : 1;
+  }
+  return p;
+}
+
+ScanArgs make_scan(const ts_chain* c, const Plan& p, const StreamWs& w, const ScanWs& sw,
+                   float* logz, uint32_t* flags) {
+  ScanArgs sa{};
+  sa.pot = c->pot;
+  sa.lengths = c->lengths;
+  sa.B = c->B;
+  sa.N = c->N;
+  sa.C = c->C;
+  sa.L = p.L;
+  sa.P = p.P;
+  sa.Ppad = p.Ppad;
+  sa.nodes = 2 * p.Ppad - 1;
+  sa.H = p.H;
+  sa.mat = sw.mat;
+  sa.off = sw.off;
+  sa.ident = sw.ident;
+  sa.cflag = sw.cflag;
+  sa.valpha = sw.valpha;
+  sa.oalpha = sw.oalpha;
+  sa.vbeta = sw.vbeta;
+  sa.obeta = sw.obeta;
+  sa.leaf_alpha = sw.leaf_alpha;
+  sa.leaf_alpha_off = sw.leaf_alpha_off;
+  sa.leaf_beta = sw.leaf_beta;
+  sa.leaf_beta_off = sw.leaf_beta_off;
+  sa.wflags = w.wflags;
+  sa.logz = logz;
+  sa.flags = flags;
+  return sa;
+}
+
+bool seg_ok(const ts_chain* c, int64_t edge_begin, int64_t n_global) {
+  return chain_ok(c) && c->lengths == nullptr && edge_begin >= 0 &&
+         edge_begin + (c->N - 1) <= n_global - 1 && c->C <= 128;
+}
+
 }  // namespace
 
 extern "C" {
@@ -341,6 +395,10 @@ TS_API size_t ts_workspace_bytes(const ts_chain* c, int op, ts_semiring s) {
     cv.take<float>((size_t)B);                 // logz
     cv.take<uint32_t>((size_t)B);              // flags
     return cv.off + op_ws(c, TS_OP_MARG, s, nullptr, nullptr, nullptr);
+  }
+  if (op == TS_OP_SEGMENT) {
+    if (c->C > 128) return 0;
+    return stream_ws(c, seg_plan(c), true, nullptr, nullptr, nullptr, true);
   }
   if (op < TS_OP_LOGZ || op > TS_OP_VITERBI) return 0;
   return op_ws(c, op, s, nullptr, nullptr, nullptr);
@@ -429,14 +487,84 @@ TS_API size_t ts_segment_summary_bytes(const ts_chain* local) {
          (size_t)(local->B * local->C) * sizeof(double);
 }
 
-TS_API ts_status ts_segment_summary(const ts_chain*, int64_t, int64_t, ts_semiring, void*, void*,
-                                    size_t, void*) {
-  return TS_E_UNSUPPORTED;  // implemented with the scan tree (scan.cu)
+TS_API ts_status ts_segment_summary(const ts_chain* local, int64_t edge_begin, int64_t n_global,
+                                    ts_semiring s, void* summary, void* ws, size_t ws_bytes,
+                                    void* stream) {
+  if (!seg_ok(local, edge_begin, n_global) || !summary || !aligned(summary, 16)) return TS_E_INVALID;
+  if (s != TS_LOG) return TS_E_UNSUPPORTED;
+  if (!device_ok()) return TS_E_UNSUPPORTED;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const Plan p = seg_plan(local);
+  StreamWs w;
+  ScanWs sw;
+  const size_t need = stream_ws(local, p, true, ws, &w, &sw, true);
+  if (ws_bytes < need || !ws || !aligned(ws, kAlign)) return TS_E_WORKSPACE;
+  cudaError_t e = cudaMemsetAsync(w.wflags, 0, sizeof(uint32_t) * (size_t)local->B, st);
+  if (e != cudaSuccess) return cuda_status(e);
+  ScanArgs sa = make_scan(local, p, w, sw, nullptr, nullptr);
+  int n = 0;
+  if ((e = launch_scan_up(sa, st, &n)) != cudaSuccess) return cuda_status(e);
+  if ((e = launch_segment_export(sa, static_cast<float*>(summary), st)) != cudaSuccess)
+    return cuda_status(e);
+  t_launches = n + 1;
+  return TS_OK;
 }
 
-TS_API ts_status ts_segment_finish(const ts_chain*, int64_t, int64_t, int, int, ts_semiring,
-                                   const void*, float*, float*, uint32_t*, void*, size_t, void*) {
-  return TS_E_UNSUPPORTED;
+TS_API ts_status ts_segment_finish(const ts_chain* local, int64_t edge_begin, int64_t n_global,
+                                   int rank, int world, ts_semiring s, const void* all_summaries,
+                                   float* marg, float* logz, uint32_t* flags, void* ws,
+                                   size_t ws_bytes, void* stream) {
+  if (!seg_ok(local, edge_begin, n_global) || !all_summaries || !logz || world < 1 || rank < 0 ||
+      rank >= world || (marg && !aligned(marg, 16)) || !aligned(all_summaries, 16))
+    return TS_E_INVALID;
+  if (s != TS_LOG) return TS_E_UNSUPPORTED;
+  if (!device_ok()) return TS_E_UNSUPPORTED;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const Plan p = seg_plan(local);
+  StreamWs w;
+  ScanWs sw;
+  const size_t need = stream_ws(local, p, true, ws, &w, &sw, true);
+  if (ws_bytes < need || !ws || !aligned(ws, kAlign)) return TS_E_WORKSPACE;
+  ScanArgs sa = make_scan(local, p, w, sw, logz, flags);
+  cudaError_t e;
+  int n = 0;
+  // prefix / suffix over the gathered segment summaries (same order on every rank) and logZ
+  if ((e = launch_segment_combine(sa, static_cast<const float*>(all_summaries), rank, world,
+                                  marg != nullptr, st)) != cudaSuccess)
+    return cuda_status(e);
+  ++n;
+  if (!marg) {
+    t_launches = n;
+    return TS_OK;
+  }
+  if ((e = launch_scan_down(sa, st, &n, false)) != cudaSuccess) return cuda_status(e);
+  SweepArgs a{};
+  a.pot = local->pot;
+  a.lengths = nullptr;
+  a.B = local->B;
+  a.N = local->N;
+  a.C = local->C;
+  a.L = p.L;
+  a.P = p.P;
+  a.alpha_in = sw.leaf_alpha;
+  a.alpha_in_off = sw.leaf_alpha_off;
+  a.beta_out = sw.leaf_beta;
+  a.beta_out_off = sw.leaf_beta_off;
+  a.alpha_hat = w.alpha_hat;
+  a.alpha_end = w.alpha_end;
+  a.alpha_end_off = w.alpha_end_off;
+  a.mlag = w.mlag;
+  a.tmax = w.tmax;
+  a.marg = marg;
+  a.wflags = w.wflags;
+  a.logz = logz;
+  a.flags = flags;
+  a.final_in_fwd = 0;
+  a.no_final = 1;
+  if ((e = launch_fwd(a, st)) != cudaSuccess) return cuda_status(e);
+  if ((e = launch_bwd(a, st)) != cudaSuccess) return cuda_status(e);
+  t_launches = n + 2;
+  return TS_OK;
 }
 
 TS_API void ts_set_plan_chunk(int64_t L) { g_plan_chunk.store(L < 0 ? 0 : L); }

@@ -272,8 +272,8 @@ __global__ void __launch_bounds__(128) bwd_sweep_kernel(SweepArgs a, int S) {
   float mu = block_max(bh, red_x, NW);
   float m = (mu == neg_inf()) ? 0.f : mu;
 
-  const bool dead = (wf & WF_NONFINITE) || (Lnext == neg_inf());
-  if (last) {  // zero the padded tail, publish logZ and flags
+  const bool dead = (wf & WF_NONFINITE) || !(Lnext > neg_inf());  // also NaN (remote segment)
+  if (last && !a.no_final) {  // zero the padded tail, publish logZ and flags
     for (int64_t q = Eb * CC + tid; q < E * CC; q += NT) mgb[q] = 0.f;
     if (tid == 0) {
       uint32_t fl = 0;
@@ -293,6 +293,8 @@ __global__ void __launch_bounds__(128) bwd_sweep_kernel(SweepArgs a, int S) {
       if (a.flags) a.flags[b] = fl;
     }
   }
+  if (last && a.no_final)
+    for (int64_t q = Eb * CC + tid; q < E * CC; q += NT) mgb[q] = 0.f;
   if (dead) {
     for (int64_t q = t0 * CC + tid; q < t1 * CC; q += NT) mgb[q] = 0.f;
     return;

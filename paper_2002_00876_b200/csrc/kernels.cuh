@@ -50,6 +50,7 @@ struct SweepArgs {
   float* logz;              // [B] (written by the last chunk's forward CTA when P == 1)
   uint32_t* flags;          // [B] or nullptr
   int final_in_fwd;         // 1: forward writes logz/flags (logZ-only call, P == 1)
+  int no_final;             // 1: backward must not write logz/flags (time-sharded segment)
 };
 size_t fwd_smem_bytes(int64_t C, int stages);
 size_t bwd_smem_bytes(int64_t C, int stages);
@@ -85,7 +86,10 @@ struct ScanArgs {
 __host__ __device__ int64_t level_off(int l, int64_t Ppad);
 size_t scan_mat_smem(int64_t C);
 cudaError_t launch_scan_up(const ScanArgs& a, cudaStream_t st, int* launches);
-cudaError_t launch_scan_down(const ScanArgs& a, cudaStream_t st, int* launches);
+cudaError_t launch_scan_down(const ScanArgs& a, cudaStream_t st, int* launches, bool set_root);
+cudaError_t launch_segment_export(const ScanArgs& a, float* summ, cudaStream_t st);
+cudaError_t launch_segment_combine(const ScanArgs& a, const float* all_summ, int rank, int world,
+                                   bool write_root, cudaStream_t st);
 cudaError_t launch_scan_logz(const ScanArgs& a, cudaStream_t st);
 
 // ---- Viterbi (max-plus) -------------------------------------------------------------

@@ -557,6 +557,121 @@ __global__ void tree_leaves_kernel(ScanArgs a) {
 }
 
 // ====================================================================================
+// Time sharding: export the local root as this segment's summary; combine
+// all gathered segment summaries into the local root vectors and the global logZ.
+// Summary layout: [B][C][C] fp32 log2 values, then [B][C] fp64 natural row offsets.
+// ====================================================================================
+__global__ void __launch_bounds__(kScanThreads) segment_export_kernel(ScanArgs a, float* summ) {
+  const int C = (int)a.C, CC = C * C;
+  const int64_t b = blockIdx.x;
+  const int64_t nr = b * a.nodes + level_off(a.H, a.Ppad);
+  float* S = summ + b * CC;
+  double* O = reinterpret_cast<double*>(summ + a.B * CC) + b * C;
+  const bool id = a.ident[nr];
+  // a NaN / +inf anywhere in this segment poisons its summary so every rank sees it
+  const bool bad = a.wflags && (a.wflags[b] & WF_NONFINITE);
+  for (int q = threadIdx.x; q < CC; q += kScanThreads)
+    S[q] = bad ? qnan() : id ? (((q / C) == (q % C)) ? 0.f : neg_inf()) : a.mat[nr * CC + q];
+  for (int r = threadIdx.x; r < C; r += kScanThreads) O[r] = id ? 0.0 : a.off[nr * C + r];
+}
+
+__global__ void __launch_bounds__(kScanThreads) segment_combine_kernel(ScanArgs a,
+                                                                       const float* all_summ,
+                                                                       int rank, int world,
+                                                                       int write_root) {
+  extern __shared__ __align__(16) float sm[];
+  const int C = (int)a.C, CC = C * C;
+  const int64_t B = a.B, b = blockIdx.x;
+  const int tid = threadIdx.x;
+  const int CC4 = (CC + 3) & ~3, C4 = (C + 3) & ~3;
+  float* S = sm;               // staged summary
+  float* va = S + CC4;         // running vector
+  float* vb = va + C4;         // output vector
+  float* scratch = vb + C4;
+  double* vo = reinterpret_cast<double*>(scratch + 4 * C4 + 32);  // [2]
+  const size_t seg_floats = (size_t)B * CC + (size_t)B * C * 2;   // fp64 offsets = 2 floats
+  auto segS = [&](int g) { return all_summ + (size_t)g * seg_floats + b * CC; };
+  auto segO = [&](int g) {
+    return reinterpret_cast<const double*>(all_summ + (size_t)g * seg_floats + B * CC) + b * C;
+  };
+  const int64_t nr = b * a.nodes + level_off(a.H, a.Ppad);
+  // a poisoned (NaN) summary anywhere -> NONFINITE on every rank, local sweeps zeroed
+  int nan = 0;
+  for (int g = 0; g < world; ++g)
+    for (int q = tid; q < CC; q += kScanThreads) nan |= (segS(g)[q] != segS(g)[q]);
+  if (__syncthreads_or(nan)) {
+    if (tid == 0) {
+      a.logz[b] = qnan();
+      if (a.flags) a.flags[b] = TS_F_NONFINITE;
+    }
+    if (write_root) {
+      for (int j = tid; j < C; j += kScanThreads) {
+        a.valpha[nr * C + j] = qnan();
+        a.vbeta[nr * C + j] = qnan();
+      }
+      if (tid == 0) {
+        a.oalpha[nr] = 0.0;
+        a.obeta[nr] = 0.0;
+      }
+    }
+    return;
+  }
+  // ---- alpha_in(rank) = 0 (x) S_0 (x) ... (x) S_{rank-1}; then the full chain for logZ ----
+  for (int j = tid; j < C; j += kScanThreads) va[j] = 0.f;
+  if (tid == 0) vo[0] = 0.0;
+  __syncthreads();
+  for (int g = 0; g < world; ++g) {
+    if (g == rank && write_root) {
+      for (int j = tid; j < C; j += kScanThreads) a.valpha[nr * C + j] = va[j];
+      if (tid == 0) a.oalpha[nr] = vo[0];
+    }
+    for (int q = tid; q < CC; q += kScanThreads) S[q] = segS(g)[q];
+    __syncthreads();
+    vec_mat(va, vo[0], S, segO(g), C, vb, &vo[1], scratch, tid);
+    for (int j = tid; j < C; j += kScanThreads) va[j] = vb[j];
+    if (tid == 0) vo[0] = vo[1];
+    __syncthreads();
+  }
+  // logZ = LSE_j(alpha_E[j]) in the same order on every rank (bit-identical across ranks)
+  if (tid == 0) {
+    float m = neg_inf();
+    bool nan = false;
+    for (int j = 0; j < C; ++j) {
+      m = fmaxf(m, va[j]);
+      nan |= (va[j] != va[j]);
+    }
+    double lz;
+    if (nan || vo[0] != vo[0]) {
+      lz = NAN;
+    } else if (m == neg_inf()) {
+      lz = -INFINITY;
+    } else {
+      double ssum = 0.0;
+      for (int j = 0; j < C; ++j) ssum += exp(kLn2 * (double)(va[j] - m));
+      lz = vo[0] + kLn2 * (double)m + log(ssum);
+    }
+    a.logz[b] = (float)lz;
+    if (a.flags) a.flags[b] = (lz != lz) ? TS_F_NONFINITE : (lz == -INFINITY ? TS_F_EMPTY : 0u);
+  }
+  if (!write_root) return;
+  // ---- beta_out(rank) = S_{rank+1} (x) ... (x) S_{world-1} (x) 0 ------------------------------
+  __syncthreads();
+  for (int j = tid; j < C; j += kScanThreads) va[j] = 0.f;
+  if (tid == 0) vo[0] = 0.0;
+  __syncthreads();
+  for (int g = world - 1; g > rank; --g) {
+    for (int q = tid; q < CC; q += kScanThreads) S[q] = segS(g)[q];
+    __syncthreads();
+    mat_vec(S, segO(g), va, vo[0], C, vb, &vo[1], scratch, tid);
+    for (int j = tid; j < C; j += kScanThreads) va[j] = vb[j];
+    if (tid == 0) vo[0] = vo[1];
+    __syncthreads();
+  }
+  for (int j = tid; j < C; j += kScanThreads) a.vbeta[nr * C + j] = va[j];
+  if (tid == 0) a.obeta[nr] = vo[0];
+}
+
+// ====================================================================================
 // host side
 // ====================================================================================
 namespace {
@@ -619,12 +734,14 @@ cudaError_t launch_scan_up(const ScanArgs& a, cudaStream_t st, int* launches) {
   return cudaSuccess;
 }
 
-cudaError_t launch_scan_down(const ScanArgs& a, cudaStream_t st, int* launches) {
+cudaError_t launch_scan_down(const ScanArgs& a, cudaStream_t st, int* launches, bool set_root) {
   cudaError_t e;
   int n = 0;
-  tree_root_kernel<<<(unsigned)a.B, 128, 0, st>>>(a);
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  ++n;
+  if (set_root) {
+    tree_root_kernel<<<(unsigned)a.B, 128, 0, st>>>(a);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    ++n;
+  }
   const size_t dsm = (size_t)(((a.C * a.C + 3) & ~3) + 4 * a.C + 32) * 4 + (size_t)(a.C + 8) * 8;
   if ((e = set_smem(tree_down_kernel, 11)) != cudaSuccess) return e;
   for (int l = a.H; l >= 1; --l) {
@@ -637,6 +754,22 @@ cudaError_t launch_scan_down(const ScanArgs& a, cudaStream_t st, int* launches) 
   ++n;
   if (launches) *launches += n;
   return cudaSuccess;
+}
+
+cudaError_t launch_segment_export(const ScanArgs& a, float* summ, cudaStream_t st) {
+  segment_export_kernel<<<(unsigned)a.B, kScanThreads, 0, st>>>(a, summ);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_segment_combine(const ScanArgs& a, const float* all_summ, int rank, int world,
+                                   bool write_root, cudaStream_t st) {
+  const int C = (int)a.C;
+  const size_t smem = (size_t)(((C * C + 3) & ~3) + 6 * ((C + 3) & ~3) + 64) * 4 + 64;
+  cudaError_t e = set_smem(segment_combine_kernel, 12);
+  if (e != cudaSuccess) return e;
+  segment_combine_kernel<<<(unsigned)a.B, kScanThreads, smem, st>>>(a, all_summ, rank, world,
+                                                                    write_root ? 1 : 0);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_scan_logz(const ScanArgs& a, cudaStream_t st) {

@@ -1,0 +1,83 @@
+"""Multi-GPU partitioning of the hot path: one process per GPU,
+torch.distributed (NCCL over NVLink / NVSwitch) for the plumbing.
+
+* Batch sharding: sequences are independent — each rank runs its contiguous slice of the
+  batch; no data-path collective (weak scaling in bench.py).
+* Time sharding (long chains, BASELINE cfg5): rank r owns a contiguous range of edges of
+  every sequence.  Each rank computes its segment's C x C transfer matrix (the semiring
+  product of its edges, the §6(a) scan applied across devices), ONE
+  all_gather_into_tensor exchanges the summaries, and every rank combines them in the same
+  order (identical logZ on all ranks) before running its local sweeps.
+
+The compute is injected (`ops`) so the host-side partitioning / gather / combine plumbing
+can be exercised on CPU with gloo in tests; the default ops are the CUDA kernels.
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+def shard_range(n: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous balanced split of n items: (begin, count) of `rank`."""
+    base, extra = divmod(int(n), int(world))
+    begin = rank * base + min(rank, extra)
+    return begin, base + (1 if rank < extra else 0)
+
+
+def shard_batch(B: int, world: int, rank: int) -> tuple[int, int]:
+    b0, nb = shard_range(B, world, rank)
+    return b0, b0 + nb
+
+
+def shard_edges(E: int, world: int, rank: int) -> tuple[int, int]:
+    """Edges [begin, begin + count) of a chain with E edges owned by `rank`."""
+    return shard_range(E, world, rank)
+
+
+class CudaSegmentOps:
+    """Default ops: the sm_100a kernels through the C ABI (ts_segment_summary/finish)."""
+
+    def __init__(self):
+        self.seg = None
+
+    def summary(self, local_pot, edge_begin, n_global):
+        from . import Segment
+
+        self.seg = Segment(local_pot, edge_begin, n_global)
+        return self.seg.summary()
+
+    def finish(self, gathered, rank, world, want_marg):
+        return self.seg.finish(gathered, rank, world, want_marg)
+
+
+def _all_gather(t: torch.Tensor, group) -> torch.Tensor:
+    world = dist.get_world_size(group)
+    out = torch.empty((world,) + tuple(t.shape), dtype=t.dtype, device=t.device)
+    try:
+        dist.all_gather_into_tensor(out, t.contiguous(), group=group)
+    except (RuntimeError, NotImplementedError, ValueError):  # backends without the fused op
+        parts = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(parts, t.contiguous(), group=group)
+        out = torch.stack(parts)
+    return out
+
+
+def time_sharded_marginals(local_pot, edge_begin: int, n_global: int, group=None,
+                           want_marg: bool = True, ops=None):
+    """Marginals / logZ of chains split in time across the ranks of `group`.
+
+    local_pot: this rank's edges [edge_begin, edge_begin + E_local) of every sequence.
+    Returns (marg for the local edges or None, logz [B] (global, identical on all ranks), flags).
+    """
+    ops = ops or CudaSegmentOps()
+    rank = dist.get_rank(group)
+    world = dist.get_world_size(group)
+    summ = ops.summary(local_pot, edge_begin, n_global)
+    gathered = _all_gather(summ, group)
+    return ops.finish(gathered, rank, world, want_marg)
+
+
+def batch_sharded(fn, pot_local, *args, **kw):
+    """Batch sharding needs no collective: each rank runs `fn` on its own slice."""
+    return fn(pot_local, *args, **kw)
