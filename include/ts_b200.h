@@ -152,6 +152,11 @@ TS_API ts_status ts_segment_finish(const ts_chain *local, int64_t edge_begin, in
 TS_API void ts_set_plan_chunk(int64_t L);
 TS_API int64_t ts_get_plan_chunk(void);
 
+/* Debug/testing knob (process-global): run short chains with C <= 32 as the chunked scan
+ * on a thread-block cluster of G CTAs per sequence exchanging chunk summaries through
+ * distributed shared memory (G in {2, 4}; 0 = the default one-CTA-per-sequence kernel). */
+TS_API void ts_set_small_cluster(int G);
+
 /* Number of kernel launches the most recent successful call on this host thread
  * enqueued (bench accounting). */
 TS_API int ts_last_launch_count(void);

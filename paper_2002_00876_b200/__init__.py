@@ -209,6 +209,11 @@ def set_plan_chunk(L: int) -> None:
     _lib.load().ts_set_plan_chunk(int(L))
 
 
+def set_small_cluster(G: int) -> None:
+    """Debug knob: short C<=32 chains on G-CTA clusters (chunked scan over DSMEM); 0 = off."""
+    _lib.load().ts_set_small_cluster(int(G))
+
+
 def get_plan_chunk() -> int:
     return int(_lib.load().ts_get_plan_chunk())
 

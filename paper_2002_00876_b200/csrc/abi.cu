@@ -14,6 +14,7 @@ using namespace tsb;
 namespace {
 
 std::atomic<int64_t> g_plan_chunk{0};
+std::atomic<int> g_small_cluster{0};  // debug: run short C<=32 chains on G-CTA clusters
 thread_local int t_launches = 0;
 
 constexpr size_t kAlign = 256;
@@ -221,7 +222,10 @@ ts_status run_log(const ts_chain* c, float* marg, float* logz, uint32_t* flags, 
   if (p.kind == PlanKind::Unsupported) return TS_E_UNSUPPORTED;
   if (p.kind == PlanKind::Small) {
     SmallArgs a{c->pot, c->lengths, c->B, c->N, c->C, marg, logz, flags};
-    ts_status r = cuda_status(launch_small(a, st));
+    const int G = g_small_cluster.load();
+    ts_status r = (G > 1 && cluster_fits(c->N, c->C, G))
+                      ? cuda_status(launch_cluster(a, G, st))
+                      : cuda_status(launch_small(a, st));
     if (r == TS_OK) t_launches = 1;
     return r;
   }
@@ -569,6 +573,9 @@ TS_API ts_status ts_segment_finish(const ts_chain* local, int64_t edge_begin, in
 
 TS_API void ts_set_plan_chunk(int64_t L) { g_plan_chunk.store(L < 0 ? 0 : L); }
 TS_API int64_t ts_get_plan_chunk(void) { return g_plan_chunk.load(); }
+TS_API void ts_set_small_cluster(int G) {
+  g_small_cluster.store((G == 2 || G == 4) ? G : 0);
+}
 TS_API int ts_last_launch_count(void) { return t_launches; }
 
 TS_API const char* ts_status_str(ts_status s) {

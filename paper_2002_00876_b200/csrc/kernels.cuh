@@ -11,7 +11,8 @@ namespace tsb {
 // Per-sequence scratch flags accumulated by the kernels that read l (device, [B]).
 enum : uint32_t { WF_NONFINITE = 2u };
 
-// ---- fused whole-sequence-in-SMEM forward/backward/marginals (C <= 32) -------------
+// ---- short chains, C <= 32: one CTA per sequence, whole chain in SMEM (fb_small.cu),
+// or the chunked-scan variant on a cluster of G CTAs per sequence (fb_cluster.cu) ---------
 struct SmallArgs {
   const float* pot;
   const int32_t* lengths;
@@ -23,6 +24,10 @@ struct SmallArgs {
 size_t small_smem_bytes(int64_t N, int64_t C);
 bool small_fits(int64_t N, int64_t C);
 cudaError_t launch_small(const SmallArgs& a, cudaStream_t st);
+int cluster_g(int64_t B, int64_t N, int sms);
+size_t cluster_smem_bytes(int64_t N, int64_t C, int G);
+bool cluster_fits(int64_t N, int64_t C, int G);
+cudaError_t launch_cluster(const SmallArgs& a, int G, cudaStream_t st);
 
 // ---- streaming (time-chunked) forward / backward sweeps, log semiring (C <= 128) ----
 // Chunk k of sequence b covers edges [k*L, min((k+1)*L, E_b)), E_b = len_b - 1.

@@ -223,3 +223,23 @@ def test_host_buffers_end_to_end(dev):
     lz_ref, mg_ref, _ = oracle.chain_marginals(pot.numpy())
     check_logz(logz.numpy(), lz_ref)
     check_marg(marg.numpy(), mg_ref)
+
+
+@pytest.mark.parametrize("G", [2, 4])
+def test_cluster_dsmem_variant(dev, G):
+    """The chunked-scan variant for short chains on a G-CTA cluster (DSMEM summary exchange)."""
+    try:
+        tsb.set_small_cluster(G)
+        for (B, N, C) in [(32, 25, 20), (3, 40, 7), (2, 17, 32)]:
+            assert_log_parity(tsgen.potentials(B, N, C, seed=G + C), None, dev)
+        pot = tsgen.tagging_potentials(6, 30, 12, seed=4, mask_frac=0.3)
+        lengths = tsgen.random_lengths(6, 30, 9)
+        pot[1] = -np.inf
+        pot[2, 5, 1, 1] = np.nan
+        lengths[3] = 1
+        lengths[4] = 0
+        assert_log_parity(pot, lengths, dev)
+        assert_log_parity(tsgen.peaked_potentials(2, 30, 20, seed=1), None, dev)
+        assert_log_parity(tsgen.large_offset_potentials(2, 30, 20, seed=2), None, dev)
+    finally:
+        tsb.set_small_cluster(0)
