@@ -26,7 +26,6 @@ __host__ __device__ inline int bwd_stride(int C, bool vec4) { return tile_stride
 __host__ __device__ inline int bwd_tile_floats(int C, bool vec4) {
   return ((C * bwd_stride(C, vec4)) + 3) & ~3;
 }
-inline int nthreads_for(int64_t C) { return (int)(((C + 31) / 32) * 32); }
 
 // block-wide max over one float per thread; `red` has >= nwarps floats; all threads get it.
 __device__ __forceinline__ float block_max(float v, float* red, int nwarps) {
@@ -62,24 +61,38 @@ __device__ __forceinline__ float block_lse2(float v, float* redm, float* reds, i
 
 }  // namespace
 
+// Thread layout (both kernels): NT = 256 threads = G groups x CW lanes, CW = C rounded up to
+// a multiple of 32.  Forward: lane j of group g owns column j, rows [g*R, g*R + R); backward:
+// lane i of group g owns row i, columns [g*R, g*R + R).  Each step: phase A (all groups,
+// partial max + partial exp-shifted sum) -> barrier -> phase B (group 0 merges the G partials
+// online-softmax style and finalises the vector) -> barrier.  Many short independent chains
+// per SM instead of one long one (latency hiding).
+constexpr int kNT = 256;
+__host__ __device__ inline int cw_of(int C) { return ((C + 31) / 32) * 32; }
+
 // ====================================================================================
 // Forward sweep
 // ====================================================================================
-template <bool VEC4>
-__global__ void __launch_bounds__(128) fwd_sweep_kernel(SweepArgs a, int S) {
+template <int CT, bool VEC4>
+__global__ void __launch_bounds__(kNT) fwd_sweep_kernel(SweepArgs a, int S) {
   extern __shared__ __align__(16) float sm[];
-  const int C = (int)a.C, CC = C * C;
+  const int C = CT > 0 ? CT : (int)a.C, CC = C * C;
   const int64_t N = a.N, E = N - 1, P = a.P, L = a.L;
   const int64_t b = blockIdx.x / P, k = blockIdx.x - (blockIdx.x / P) * P;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int NT = blockDim.x, NW = NT >> 5;
+  constexpr int NW = kNT / 32;
+  const int CW = cw_of(C), G = kNT / CW, NW0 = CW / 32;
+  const int g = tid / CW, j = tid - g * CW;
+  const int R = (C + G - 1) / G, r0 = g * R, r1 = min(C, r0 + R);
   const int TF = fwd_tile_floats(C);
   float* ring = sm;
-  float* a_s = ring + (size_t)S * TF;  // [2][NT]
-  float* ah_s = a_s + 2 * NT;          // [2][NT]
-  float* red_mu = ah_s + 2 * NT;       // [2][NW]
-  float* red_T = red_mu + 2 * NW;      // [NW]
-  float* red_x = red_T + NW;           // [2*NW] scratch
+  float* a_s = ring + (size_t)S * TF;  // [2][CW]
+  float* ah_s = a_s + 2 * CW;          // [2][CW]
+  float* pm = ah_s + 2 * CW;           // [G][CW] partial column max
+  float* ps = pm + kNT;                // [G][CW] partial sums
+  float* red_T = ps + kNT;             // [NW]
+  float* red_mu = red_T + NW;          // [2][NW]
+  float* red_x = red_mu + 2 * NW;      // [2*NW]
 
   const int64_t len = seq_len(a.lengths, b, N);
   if (len < 0) {
@@ -95,25 +108,27 @@ __global__ void __launch_bounds__(128) fwd_sweep_kernel(SweepArgs a, int S) {
   const int64_t t1 = (t0 + L < Eb) ? t0 + L : Eb;
   const int64_t nsteps = t1 - t0;
   const bool last = (t1 == Eb);
-  const bool act = tid < C;
+  const bool act = (j < C);          // this lane's column exists
+  const bool own = act && (g == 0);  // finalises column j
   const int64_t bk = b * P + k;
   const float* potb = a.pot + b * E * (int64_t)CC;
 
   // start vector (chunk 0: log-one; otherwise alpha_in from the scan tree)
-  float ah = act ? (a.alpha_in ? a.alpha_in[bk * C + tid] : 0.f) : neg_inf();
+  float ah = own ? (a.alpha_in ? a.alpha_in[bk * C + j] : 0.f) : neg_inf();
   double O = a.alpha_in_off ? a.alpha_in_off[bk] : 0.0;
   float mu = block_max(ah, red_x, NW);
   float m = (mu == neg_inf()) ? 0.f : mu;
-  if (a.alpha_hat && act) a.alpha_hat[(b * N + t0) * C + tid] = ah;
+  if (a.alpha_hat && own) a.alpha_hat[(b * N + t0) * C + j] = ah;
 
-  // prologue: stage the first S-1 tiles
   for (int u = 0; u < S - 1; ++u) {
     if (u < nsteps)
-      stage_tile(ring + (size_t)(u % S) * TF, potb + (t0 + u) * (int64_t)CC, C, C, VEC4, tid, NT);
+      stage_tile(ring + (size_t)(u % S) * TF, potb + (t0 + u) * (int64_t)CC, C, C, VEC4, tid, kNT);
     cp_async_commit();
   }
-  a_s[tid] = act ? ex2(ah - m) : 0.f;
-  ah_s[tid] = ah;
+  if (g == 0) {
+    a_s[j] = own ? ex2(ah - m) : 0.f;
+    ah_s[j] = ah;
+  }
   cp_async_wait_dyn(S - 2);
   __syncthreads();
 
@@ -126,83 +141,107 @@ __global__ void __launch_bounds__(128) fwd_sweep_kernel(SweepArgs a, int S) {
       const int64_t uu = u + S - 1;
       if (uu < nsteps)
         stage_tile(ring + (size_t)(uu % S) * TF, potb + (t0 + uu) * (int64_t)CC, C, C, VEC4, tid,
-                   NT);
+                   kNT);
       cp_async_commit();
     }
     const float* tile = ring + (size_t)(u % S) * TF;
-    const float* av = a_s + buf * NT;
-    // ---- phase A: column max and exp-shifted dot product --------------------------
+    const float* av = a_s + buf * CW;
+    // ---- phase A: partial column max and exp-shifted partial dot product -------------------
     float M = neg_inf(), s = 0.f;
-    if (act) {
-      for (int i = 0; i < C; ++i) M = fmaxf(M, tile[i * C + tid]);
+    if (act && r0 < r1) {
+      float m0 = neg_inf(), m1 = neg_inf();
+      int i = r0;
+      for (; i + 2 <= r1; i += 2) {
+        m0 = fmaxf(m0, tile[i * C + j]);
+        m1 = fmaxf(m1, tile[(i + 1) * C + j]);
+      }
+      if (i < r1) m0 = fmaxf(m0, tile[i * C + j]);
+      M = fmaxf(m0, m1);
       if (M != neg_inf()) {
         float s0 = 0.f, s1 = 0.f;
-        int i = 0;
-        for (; i + 2 <= C; i += 2) {
-          s0 = fmaf(av[i], ex2((tile[i * C + tid] - M) * kLog2e), s0);
-          s1 = fmaf(av[i + 1], ex2((tile[(i + 1) * C + tid] - M) * kLog2e), s1);
+        i = r0;
+        for (; i + 2 <= r1; i += 2) {
+          s0 = fmaf(av[i], ex2((tile[i * C + j] - M) * kLog2e), s0);
+          s1 = fmaf(av[i + 1], ex2((tile[(i + 1) * C + j] - M) * kLog2e), s1);
         }
-        if (i < C) s0 = fmaf(av[i], ex2((tile[i * C + tid] - M) * kLog2e), s0);
+        if (i < r1) s0 = fmaf(av[i], ex2((tile[i * C + j] - M) * kLog2e), s0);
         s = s0 + s1;
       }
     }
+    pm[g * CW + j] = M;
+    ps[g * CW + j] = s;
     {
-      float wm = warp_max(M);
+      const float wm = warp_max(M);
       if (lane == 0) red_T[w] = wm;
     }
     __syncthreads();
     float T = red_T[0];
+#pragma unroll
     for (int q = 1; q < NW; ++q) T = fmaxf(T, red_T[q]);
     const float Tz = (T == neg_inf()) ? 0.f : T;
-    // ---- phase B: finalise ah_{t+1}[j] -------------------------------------------------
-    float nh = neg_inf();
-    if (act && M != neg_inf()) {
-      nh = (M - Tz) * kLog2e + lg2(s);
-      if (!(s >= kGate)) {  // exact per-cell-max path (also reached by NaN)
-        const float* ahv = ah_s + buf * NT;
-        float q = neg_inf();
-        for (int i = 0; i < C; ++i) q = fmaxf(q, ahv[i] + (tile[i * C + tid] - Tz) * kLog2e);
-        if (q == neg_inf()) {
-          nh = neg_inf();
-        } else {
-          float ss = 0.f;
-          for (int i = 0; i < C; ++i) ss += ex2(ahv[i] + (tile[i * C + tid] - Tz) * kLog2e - q);
-          nh = q + lg2(ss) - m;
+    const float m_next = (mu == neg_inf()) ? 0.f : (log2C + mu - m);
+    // ---- phase B: every group merges the G partials of its column (redundantly, no idle
+    // warps); group 0 finalises ah_{t+1}[j] ---------------------------------------------------
+    {
+      float nh = neg_inf();
+      if (act) {
+        float Mj = neg_inf();
+        for (int q = 0; q < G; ++q) Mj = fmaxf(Mj, pm[q * CW + j]);
+        if (Mj != neg_inf()) {
+          float sj = 0.f;
+          for (int q = 0; q < G; ++q) {
+            const float mq = pm[q * CW + j];
+            if (mq != neg_inf()) sj = fmaf(ps[q * CW + j], ex2((mq - Mj) * kLog2e), sj);
+          }
+          nh = (Mj - Tz) * kLog2e + lg2(sj);
+          if (g == 0 && !(sj >= kGate)) {  // exact per-cell-max path (also reached by NaN)
+            const float* ahv = ah_s + buf * CW;
+            float q = neg_inf();
+            for (int i = 0; i < C; ++i) q = fmaxf(q, ahv[i] + (tile[i * C + j] - Tz) * kLog2e);
+            if (q == neg_inf()) {
+              nh = neg_inf();
+            } else {
+              float ss = 0.f;
+              for (int i = 0; i < C; ++i) ss += ex2(ahv[i] + (tile[i * C + j] - Tz) * kLog2e - q);
+              nh = q + lg2(ss) - m;
+            }
+            if (sj != sj) nh = qnan();
+          }
         }
-        if (s != s) nh = qnan();
+        if (g == 0) {
+          if (nh != nh || Mj == pos_inf()) bad = 1u;
+          if (a.alpha_hat && t + 1 < t1) a.alpha_hat[(b * N + t + 1) * C + j] = nh;
+        }
+      }
+      if (g == 0) {
+        ah_s[(buf ^ 1) * CW + j] = nh;
+        a_s[(buf ^ 1) * CW + j] = act ? ex2(nh - m_next) : 0.f;
+        const float wm = warp_max(nh);
+        if (lane == 0) red_mu[(buf ^ 1) * NW + w] = wm;
+        ah = nh;
       }
     }
-    if (nh != nh || M == pos_inf()) bad = 1u;
-    if (a.alpha_hat && act && t + 1 < t1) a.alpha_hat[(b * N + t + 1) * C + tid] = nh;
     if (tid == 0) {
       if (a.mlag) a.mlag[b * N + t] = m;
       if (a.tmax) a.tmax[b * E + t] = Tz;
     }
     O += kLn2 * (double)m + (double)Tz;
-    const float m_next = (mu == neg_inf()) ? 0.f : (log2C + mu - m);
-    ah_s[(buf ^ 1) * NT + tid] = nh;
-    a_s[(buf ^ 1) * NT + tid] = act ? ex2(nh - m_next) : 0.f;
-    {
-      float wm = warp_max(nh);
-      if (lane == 0) red_mu[(buf ^ 1) * NW + w] = wm;
-    }
     cp_async_wait_dyn(S - 2);
     __syncthreads();
     float mx = red_mu[(buf ^ 1) * NW];
-    for (int q = 1; q < NW; ++q) mx = fmaxf(mx, red_mu[(buf ^ 1) * NW + q]);
+    for (int q = 1; q < NW0; ++q) mx = fmaxf(mx, red_mu[(buf ^ 1) * NW + q]);
     mu = mx;
     m = m_next;
-    ah = nh;
     buf ^= 1;
   }
   cp_async_wait<0>();
-  if (a.alpha_end && act) a.alpha_end[bk * C + tid] = ah;
+  if (a.alpha_end && own) a.alpha_end[bk * C + j] = ah;
   if (a.alpha_end_off && tid == 0) a.alpha_end_off[bk] = O;
   // NONFINITE: any NaN/+inf propagates to a NaN column (0 * NaN = NaN in the dot product)
   const unsigned anybad = __syncthreads_or(bad);
   if (anybad && tid == 0 && a.wflags) atomicOr(&a.wflags[b], (unsigned)WF_NONFINITE);
   if (a.final_in_fwd && last) {
-    const float Lz = block_lse2(act ? ah : neg_inf(), red_x, red_x + NW, NW);
+    const float Lz = block_lse2(own ? ah : neg_inf(), red_x, red_x + NW, NW);
     if (tid == 0) {
       uint32_t fl = 0;
       float lz;
@@ -224,20 +263,27 @@ __global__ void __launch_bounds__(128) fwd_sweep_kernel(SweepArgs a, int S) {
 // ====================================================================================
 // Backward sweep + marginals
 // ====================================================================================
-template <bool VEC4>
-__global__ void __launch_bounds__(128) bwd_sweep_kernel(SweepArgs a, int S) {
+template <int CT, bool VEC4>
+__global__ void __launch_bounds__(kNT) bwd_sweep_kernel(SweepArgs a, int S) {
   extern __shared__ __align__(16) float sm[];
-  const int C = (int)a.C, CC = C * C;
+  const int C = CT > 0 ? CT : (int)a.C, CC = C * C;
   const int64_t N = a.N, E = N - 1, P = a.P, L = a.L;
   const int64_t b = blockIdx.x / P, k = blockIdx.x - (blockIdx.x / P) * P;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int NT = blockDim.x, NW = NT >> 5;
+  constexpr int NW = kNT / 32;
+  const int CW = cw_of(C), G = kNT / CW, NW0 = CW / 32;
+  const int g = tid / CW, i = tid - g * CW;
+  int R = (C + G - 1) / G;
+  if (VEC4) R = (R + 3) & ~3;
+  const int c0 = min(C, g * R), c1 = min(C, c0 + R);
   const int SB = bwd_stride(C, VEC4);
   const int TF = bwd_tile_floats(C, VEC4);
   float* ring = sm;
-  float* b_s = ring + (size_t)S * TF;  // [2][NT] b values
-  float* bh_s = b_s + 2 * NT;          // [2][NT] bh values
-  float* red_mu = bh_s + 2 * NT;       // [2][NW]
+  float* b_s = ring + (size_t)S * TF;  // [2][CW] b values
+  float* bh_s = b_s + 2 * CW;          // [2][CW] bh values
+  float* pr = bh_s + 2 * CW;           // [G][CW] partial row max
+  float* ps = pr + kNT;                // [G][CW] partial sums
+  float* red_mu = ps + kNT;            // [2][NW]
   float* red_lm = red_mu + 2 * NW;     // [2][NW]
   float* red_ls = red_lm + 2 * NW;     // [2][NW]
   float* red_x = red_ls + 2 * NW;      // [2*NW]
@@ -246,7 +292,7 @@ __global__ void __launch_bounds__(128) bwd_sweep_kernel(SweepArgs a, int S) {
   float* mgb = a.marg + b * E * (int64_t)CC;
   if (len < 0) {  // BADLEN: chunk 0 zeroes everything
     if (k == 0) {
-      for (int64_t q = tid; q < E * CC; q += NT) mgb[q] = 0.f;
+      for (int64_t q = tid; q < E * CC; q += kNT) mgb[q] = 0.f;
       if (tid == 0) {
         a.logz[b] = qnan();
         if (a.flags) a.flags[b] = TS_F_BADLEN;
@@ -260,21 +306,22 @@ __global__ void __launch_bounds__(128) bwd_sweep_kernel(SweepArgs a, int S) {
   const int64_t t1 = (t0 + L < Eb) ? t0 + L : Eb;
   const int64_t nsteps = t1 - t0;
   const bool last = (t1 == Eb);
-  const bool act = tid < C;
+  const bool act = (i < C);
+  const bool own = act && (g == 0);
   const int64_t bk = b * P + k;
   const float* potb = a.pot + b * E * (int64_t)CC;
   const uint32_t wf = a.wflags ? a.wflags[b] : 0u;
 
   // end-of-chunk vectors: beta_out (tree) or log-one; alpha in the chunk's own frame
-  float bh = act ? (a.beta_out ? a.beta_out[bk * C + tid] : 0.f) : neg_inf();
-  const float ahe = act ? a.alpha_end[bk * C + tid] : neg_inf();
-  float Lnext = block_lse2(act ? ahe + bh : neg_inf(), red_x, red_x + NW, NW);
+  float bh = own ? (a.beta_out ? a.beta_out[bk * C + i] : 0.f) : neg_inf();
+  const float ahe = own ? a.alpha_end[bk * C + i] : neg_inf();
+  float Lnext = block_lse2(own ? ahe + bh : neg_inf(), red_x, red_x + NW, NW);
   float mu = block_max(bh, red_x, NW);
   float m = (mu == neg_inf()) ? 0.f : mu;
 
   const bool dead = (wf & WF_NONFINITE) || !(Lnext > neg_inf());  // also NaN (remote segment)
   if (last && !a.no_final) {  // zero the padded tail, publish logZ and flags
-    for (int64_t q = Eb * CC + tid; q < E * CC; q += NT) mgb[q] = 0.f;
+    for (int64_t q = Eb * CC + tid; q < E * CC; q += kNT) mgb[q] = 0.f;
     if (tid == 0) {
       uint32_t fl = 0;
       float lz;
@@ -294,101 +341,119 @@ __global__ void __launch_bounds__(128) bwd_sweep_kernel(SweepArgs a, int S) {
     }
   }
   if (last && a.no_final)
-    for (int64_t q = Eb * CC + tid; q < E * CC; q += NT) mgb[q] = 0.f;
+    for (int64_t q = Eb * CC + tid; q < E * CC; q += kNT) mgb[q] = 0.f;
   if (dead) {
-    for (int64_t q = t0 * CC + tid; q < t1 * CC; q += NT) mgb[q] = 0.f;
+    for (int64_t q = t0 * CC + tid; q < t1 * CC; q += kNT) mgb[q] = 0.f;
     return;
   }
 
   for (int u = 0; u < S - 1; ++u) {
     if (u < nsteps)
-      stage_tile(ring + (size_t)(u % S) * TF, potb + (t1 - 1 - u) * (int64_t)CC, C, SB, VEC4,
-                 tid, NT);
+      stage_tile(ring + (size_t)(u % S) * TF, potb + (t1 - 1 - u) * (int64_t)CC, C, SB, VEC4, tid,
+                 kNT);
     cp_async_commit();
   }
-  b_s[tid] = act ? ex2(bh - m) : 0.f;
-  bh_s[tid] = bh;
+  if (g == 0) {
+    b_s[i] = own ? ex2(bh - m) : 0.f;
+    bh_s[i] = bh;
+  }
   cp_async_wait_dyn(S - 2);
   __syncthreads();
 
   const float log2C = lg2((float)C);
   int buf = 0;
+  float aht = (act && nsteps > 0) ? a.alpha_hat[(b * N + t1 - 1) * C + i] : neg_inf();
   for (int64_t u = 0; u < nsteps; ++u) {
     const int64_t t = t1 - 1 - u;
     {
       const int64_t uu = u + S - 1;
       if (uu < nsteps)
         stage_tile(ring + (size_t)(uu % S) * TF, potb + (t1 - 1 - uu) * (int64_t)CC, C, SB, VEC4,
-                   tid, NT);
+                   tid, kNT);
       cp_async_commit();
     }
     const float* tile = ring + (size_t)(u % S) * TF;
-    const float* bv = b_s + buf * NT;
-    const float* bhv = bh_s + buf * NT;
+    const float* bv = b_s + buf * CW;
+    const float* bhv = bh_s + buf * CW;
     const float Tt = a.tmax[b * E + t];
     const float mt = a.mlag[b * N + t];
-    float aht = act ? a.alpha_hat[(b * N + t) * C + tid] : neg_inf();
-    float nb = neg_inf();
-    if (act) {
-      const float* row = tile + tid * SB;
-      float* mrow = mgb + ((int64_t)t * C + tid) * C;
-      const float cst = aht - mt - Lnext;
-      float R = neg_inf();
-      float s = 0.f;
+    const float aht_cur = aht;
+    if (act && u + 1 < nsteps) aht = a.alpha_hat[(b * N + t - 1) * C + i];  // prefetch
+    // ---- phase A: partial row max, partial sum, and this group's marginals ------------------
+    float Rg = neg_inf(), s = 0.f;
+    if (act && c0 < c1) {
+      const float* row = tile + i * SB;
+      float* mrow = mgb + ((int64_t)t * C + i) * C;
+      const float cst = aht_cur - mt - Lnext;
       if (VEC4) {
-        for (int j = 0; j < C; j += 4) {
-          float4 v = *reinterpret_cast<const float4*>(row + j);
-          R = fmaxf(R, fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)));
+        for (int c = c0; c < c1; c += 4) {
+          const float4 v = *reinterpret_cast<const float4*>(row + c);
+          Rg = fmaxf(Rg, fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)));
         }
-        for (int j = 0; j < C; j += 4) {
-          const float4 v = *reinterpret_cast<const float4*>(row + j);
-          const float4 bb = *reinterpret_cast<const float4*>(bv + j);
-          const float4 hh = *reinterpret_cast<const float4*>(bhv + j);
-          if (R != neg_inf()) {
-            s = fmaf(ex2((v.x - R) * kLog2e), bb.x, s);
-            s = fmaf(ex2((v.y - R) * kLog2e), bb.y, s);
-            s = fmaf(ex2((v.z - R) * kLog2e), bb.z, s);
-            s = fmaf(ex2((v.w - R) * kLog2e), bb.w, s);
+        for (int c = c0; c < c1; c += 4) {
+          const float4 v = *reinterpret_cast<const float4*>(row + c);
+          const float4 bb = *reinterpret_cast<const float4*>(bv + c);
+          const float4 hh = *reinterpret_cast<const float4*>(bhv + c);
+          if (Rg != neg_inf()) {
+            s = fmaf(ex2((v.x - Rg) * kLog2e), bb.x, s);
+            s = fmaf(ex2((v.y - Rg) * kLog2e), bb.y, s);
+            s = fmaf(ex2((v.z - Rg) * kLog2e), bb.z, s);
+            s = fmaf(ex2((v.w - Rg) * kLog2e), bb.w, s);
           }
           float4 mu4;
           mu4.x = ex2(cst + hh.x + (v.x - Tt) * kLog2e);
           mu4.y = ex2(cst + hh.y + (v.y - Tt) * kLog2e);
           mu4.z = ex2(cst + hh.z + (v.z - Tt) * kLog2e);
           mu4.w = ex2(cst + hh.w + (v.w - Tt) * kLog2e);
-          *reinterpret_cast<float4*>(mrow + j) = mu4;
+          *reinterpret_cast<float4*>(mrow + c) = mu4;
         }
       } else {
-        for (int j = 0; j < C; ++j) R = fmaxf(R, row[j]);
-        for (int j = 0; j < C; ++j) {
-          const float v = row[j];
-          if (R != neg_inf()) s = fmaf(ex2((v - R) * kLog2e), bv[j], s);
-          mrow[j] = ex2(cst + bhv[j] + (v - Tt) * kLog2e);
-        }
-      }
-      if (R != neg_inf()) {
-        nb = (R - Tt) * kLog2e + lg2(s);
-        if (!(s >= kGate)) {  // exact per-cell-max path
-          float q = neg_inf();
-          for (int j = 0; j < C; ++j) q = fmaxf(q, (row[j] - Tt) * kLog2e + bhv[j]);
-          if (q == neg_inf()) {
-            nb = neg_inf();
-          } else {
-            float ss = 0.f;
-            for (int j = 0; j < C; ++j) ss += ex2((row[j] - Tt) * kLog2e + bhv[j] - q);
-            nb = q + lg2(ss) - m;
-          }
+        for (int c = c0; c < c1; ++c) Rg = fmaxf(Rg, row[c]);
+        for (int c = c0; c < c1; ++c) {
+          const float v = row[c];
+          if (Rg != neg_inf()) s = fmaf(ex2((v - Rg) * kLog2e), bv[c], s);
+          mrow[c] = ex2(cst + bhv[c] + (v - Tt) * kLog2e);
         }
       }
     }
+    pr[g * CW + i] = Rg;
+    ps[g * CW + i] = s;
+    __syncthreads();
     const float m_next = (mu == neg_inf()) ? 0.f : (log2C + mu - m);
-    b_s[(buf ^ 1) * NT + tid] = act ? ex2(nb - m_next) : 0.f;
-    bh_s[(buf ^ 1) * NT + tid] = nb;
-    {
-      float wm = warp_max(nb);
-      const float v = act ? aht + nb : neg_inf();
-      float lm = warp_max(v);
-      float le = (lm == neg_inf()) ? 0.f : ex2(v - lm);
-      float ls = warp_sum(le);
+    // ---- phase B (group 0): merge, finalise bh_t[i], reductions for the next step -----------
+    if (g == 0) {
+      float nb = neg_inf();
+      if (act) {
+        float Ri = neg_inf();
+        for (int q = 0; q < G; ++q) Ri = fmaxf(Ri, pr[q * CW + i]);
+        if (Ri != neg_inf()) {
+          float si = 0.f;
+          for (int q = 0; q < G; ++q) {
+            const float rq = pr[q * CW + i];
+            if (rq != neg_inf()) si = fmaf(ps[q * CW + i], ex2((rq - Ri) * kLog2e), si);
+          }
+          nb = (Ri - Tt) * kLog2e + lg2(si);
+          if (!(si >= kGate)) {  // exact per-cell-max path
+            const float* row = tile + i * SB;
+            float q = neg_inf();
+            for (int c = 0; c < C; ++c) q = fmaxf(q, (row[c] - Tt) * kLog2e + bhv[c]);
+            if (q == neg_inf()) {
+              nb = neg_inf();
+            } else {
+              float ss = 0.f;
+              for (int c = 0; c < C; ++c) ss += ex2((row[c] - Tt) * kLog2e + bhv[c] - q);
+              nb = q + lg2(ss) - m;
+            }
+          }
+        }
+      }
+      b_s[(buf ^ 1) * CW + i] = act ? ex2(nb - m_next) : 0.f;
+      bh_s[(buf ^ 1) * CW + i] = nb;
+      const float wm = warp_max(nb);
+      const float v = act ? aht_cur + nb : neg_inf();
+      const float lm = warp_max(v);
+      const float le = (lm == neg_inf()) ? 0.f : ex2(v - lm);
+      const float ls = warp_sum(le);
       if (lane == 0) {
         red_mu[(buf ^ 1) * NW + w] = wm;
         red_lm[(buf ^ 1) * NW + w] = lm;
@@ -402,13 +467,13 @@ __global__ void __launch_bounds__(128) bwd_sweep_kernel(SweepArgs a, int S) {
       const float* lmv = red_lm + (buf ^ 1) * NW;
       const float* lsv = red_ls + (buf ^ 1) * NW;
       float mx = rm[0], LM = lmv[0];
-      for (int q = 1; q < NW; ++q) {
+      for (int q = 1; q < NW0; ++q) {
         mx = fmaxf(mx, rm[q]);
         LM = fmaxf(LM, lmv[q]);
       }
       float LS = 0.f;
       if (LM != neg_inf())
-        for (int q = 0; q < NW; ++q) LS += (lmv[q] == neg_inf()) ? 0.f : lsv[q] * ex2(lmv[q] - LM);
+        for (int q = 0; q < NW0; ++q) LS += (lmv[q] == neg_inf()) ? 0.f : lsv[q] * ex2(lmv[q] - LM);
       Lnext = (LM == neg_inf()) ? neg_inf() : LM + lg2(LS);
       mu = mx;
     }
@@ -440,7 +505,7 @@ template <typename K>
 cudaError_t set_smem_once(K kern, std::atomic<uint64_t>& mask, int bit) {
   int dev = 0;
   cudaGetDevice(&dev);
-  const uint64_t m = 1ull << ((dev & 15) * 4 + bit);
+  const uint64_t m = 1ull << ((dev & 7) * 8 + bit);
   if (mask.load() & m) return cudaSuccess;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
   if (e == cudaSuccess) mask.fetch_or(m);
@@ -449,47 +514,59 @@ cudaError_t set_smem_once(K kern, std::atomic<uint64_t>& mask, int bit) {
 }  // namespace
 
 size_t fwd_smem_bytes(int64_t C, int stages) {
-  const int NT = nthreads_for(C), NW = NT / 32;
-  return ((size_t)stages * fwd_tile_floats((int)C) + 4 * NT + 5 * NW) * sizeof(float);
+  const int CW = cw_of((int)C), NW = kNT / 32;
+  return ((size_t)stages * fwd_tile_floats((int)C) + 4 * CW + 2 * kNT + 5 * NW) * sizeof(float);
 }
 size_t bwd_smem_bytes(int64_t C, int stages) {
   const bool vec4 = (C % 4) == 0;
-  const int NT = nthreads_for(C), NW = NT / 32;
-  return ((size_t)stages * bwd_tile_floats((int)C, vec4) + 4 * NT + 8 * NW) * sizeof(float);
+  const int CW = cw_of((int)C), NW = kNT / 32;
+  return ((size_t)stages * bwd_tile_floats((int)C, vec4) + 4 * CW + 2 * kNT + 8 * NW) * sizeof(float);
 }
 
 cudaError_t launch_fwd(const SweepArgs& a, cudaStream_t st) {
+  if (stream2_ok(a)) return launch_fwd2(a, st);
   const int C = (int)a.C;
   const bool vec4 = (C % 4) == 0 && (reinterpret_cast<uintptr_t>(a.pot) & 15) == 0;
   const int S = fwd_stages(C);
   const size_t smem = fwd_smem_bytes(C, S);
-  const dim3 grid((unsigned)(a.B * a.P)), block(nthreads_for(C));
+  const dim3 grid((unsigned)(a.B * a.P)), block(kNT);
   cudaError_t e;
-  if (vec4) {
-    if ((e = set_smem_once(fwd_sweep_kernel<true>, g_attr_fwd, 0)) != cudaSuccess) return e;
-    fwd_sweep_kernel<true><<<grid, block, smem, st>>>(a, S);
-  } else {
-    if ((e = set_smem_once(fwd_sweep_kernel<false>, g_attr_fwd, 1)) != cudaSuccess) return e;
-    fwd_sweep_kernel<false><<<grid, block, smem, st>>>(a, S);
-  }
+#define TS_FWD(CTV, V4, BIT)                                                                \
+  do {                                                                                   \
+    if ((e = set_smem_once(fwd_sweep_kernel<CTV, V4>, g_attr_fwd, BIT)) != cudaSuccess) \
+      return e;                                                                          \
+    fwd_sweep_kernel<CTV, V4><<<grid, block, smem, st>>>(a, S);                          \
+  } while (0)
+  if (vec4 && C == 64) TS_FWD(64, true, 0);
+  else if (vec4 && C == 128) TS_FWD(128, true, 1);
+  else if (vec4 && C == 32) TS_FWD(32, true, 2);
+  else if (vec4) TS_FWD(0, true, 3);
+  else TS_FWD(0, false, 4);
+#undef TS_FWD
   return cudaGetLastError();
 }
 
 cudaError_t launch_bwd(const SweepArgs& a, cudaStream_t st) {
+  if (stream2_ok(a)) return launch_bwd2(a, st);
   const int C = (int)a.C;
   const bool vec4 = (C % 4) == 0 && (reinterpret_cast<uintptr_t>(a.pot) & 15) == 0 &&
                     (reinterpret_cast<uintptr_t>(a.marg) & 15) == 0;
   const int S = bwd_stages(C, vec4);
   const size_t smem = bwd_smem_bytes(C, S);
-  const dim3 grid((unsigned)(a.B * a.P)), block(nthreads_for(C));
+  const dim3 grid((unsigned)(a.B * a.P)), block(kNT);
   cudaError_t e;
-  if (vec4) {
-    if ((e = set_smem_once(bwd_sweep_kernel<true>, g_attr_bwd, 0)) != cudaSuccess) return e;
-    bwd_sweep_kernel<true><<<grid, block, smem, st>>>(a, S);
-  } else {
-    if ((e = set_smem_once(bwd_sweep_kernel<false>, g_attr_bwd, 1)) != cudaSuccess) return e;
-    bwd_sweep_kernel<false><<<grid, block, smem, st>>>(a, S);
-  }
+#define TS_BWD(CTV, V4, BIT)                                                                \
+  do {                                                                                   \
+    if ((e = set_smem_once(bwd_sweep_kernel<CTV, V4>, g_attr_bwd, BIT)) != cudaSuccess) \
+      return e;                                                                          \
+    bwd_sweep_kernel<CTV, V4><<<grid, block, smem, st>>>(a, S);                          \
+  } while (0)
+  if (vec4 && C == 64) TS_BWD(64, true, 0);
+  else if (vec4 && C == 128) TS_BWD(128, true, 1);
+  else if (vec4 && C == 32) TS_BWD(32, true, 2);
+  else if (vec4) TS_BWD(0, true, 3);
+  else TS_BWD(0, false, 4);
+#undef TS_BWD
   return cudaGetLastError();
 }
 

@@ -61,6 +61,10 @@ size_t fwd_smem_bytes(int64_t C, int stages);
 size_t bwd_smem_bytes(int64_t C, int stages);
 cudaError_t launch_fwd(const SweepArgs& a, cudaStream_t st);
 cudaError_t launch_bwd(const SweepArgs& a, cudaStream_t st);
+// register-blocked variants for C in {32, 64, 128} (fb_stream2.cu)
+bool stream2_ok(const SweepArgs& a);
+cudaError_t launch_fwd2(const SweepArgs& a, cudaStream_t st);
+cudaError_t launch_bwd2(const SweepArgs& a, cudaStream_t st);
 
 // ---- time-chunked scan (scan.cu): leaf summaries, up-sweep tree, down-sweep ---------
 // Tree of one sequence: levels 0..H, level l holds Ppad >> l nodes (Ppad = 2^H >= P),
