@@ -15,8 +15,14 @@ all: $(PKG)/libts_b200.so infra
 
 infra: tsgen/libtsgen_host.so tsgen/libtsgen_device.so oracle/liboracle.so
 
-$(PKG)/libts_b200.so: $(KERN_SRCS) $(KERN_HDRS)
-	$(NVCC) $(NVFLAGS) -Iinclude -shared -o $@ $(KERN_SRCS) -lcuda
+KERN_OBJS := $(patsubst $(CSRC)/%.cu,build/%.o,$(KERN_SRCS))
+
+build/%.o: $(CSRC)/%.cu $(KERN_HDRS)
+	@mkdir -p build
+	$(NVCC) $(NVFLAGS) -Iinclude -c -o $@ $<
+
+$(PKG)/libts_b200.so: $(KERN_OBJS)
+	$(NVCC) $(NVFLAGS) -shared -o $@ $(KERN_OBJS) -lcuda
 
 tsgen/libtsgen_device.so: tsgen/tsgen_device.cu tsgen/tsgen.h
 	$(NVCC) $(NVFLAGS) -shared -o $@ tsgen/tsgen_device.cu
@@ -29,5 +35,6 @@ oracle/liboracle.so: oracle/oracle.c tsgen/tsgen.h
 
 clean:
 	rm -f $(PKG)/libts_b200.so tsgen/*.so oracle/*.so
+	rm -rf build
 
 .PHONY: all infra clean

@@ -157,6 +157,12 @@ TS_API int64_t ts_get_plan_chunk(void);
  * distributed shared memory (G in {2, 4}; 0 = the default one-CTA-per-sequence kernel). */
 TS_API void ts_set_small_cluster(int G);
 
+/* Debug/testing knob (process-global): 1 (default) runs ts_marginals for C = 64 with one
+ * serial chunk per sequence as the meet-in-the-middle kernel (forward and backward
+ * recursions concurrently from both ends, marginals fused); 0 = separate forward and
+ * backward sweep kernels.  Results agree within the parity tolerances. */
+TS_API void ts_set_meet(int enable);
+
 /* Number of kernel launches the most recent successful call on this host thread
  * enqueued (bench accounting). */
 TS_API int ts_last_launch_count(void);

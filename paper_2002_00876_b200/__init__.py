@@ -214,6 +214,11 @@ def set_small_cluster(G: int) -> None:
     _lib.load().ts_set_small_cluster(int(G))
 
 
+def set_meet(enable: bool) -> None:
+    """Debug knob: meet-in-the-middle fused marginals kernel for C = 64 (default on)."""
+    _lib.load().ts_set_meet(1 if enable else 0)
+
+
 def get_plan_chunk() -> int:
     return int(_lib.load().ts_get_plan_chunk())
 

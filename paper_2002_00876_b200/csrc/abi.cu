@@ -14,7 +14,8 @@ using namespace tsb;
 namespace {
 
 std::atomic<int64_t> g_plan_chunk{0};
-std::atomic<int> g_small_cluster{0};  // debug: run short C<=32 chains on G-CTA clusters
+std::atomic<int> g_small_cluster{0};
+std::atomic<int> g_meet{1};  // meet-in-the-middle marginals kernel for C = 64  // debug: run short C<=32 chains on G-CTA clusters
 thread_local int t_launches = 0;
 
 constexpr size_t kAlign = 256;
@@ -126,6 +127,7 @@ struct StreamWs {
   float* alpha_end = nullptr;
   double* alpha_end_off = nullptr;
   uint32_t* wflags = nullptr;
+  float* beta_hat = nullptr;  // meet-in-the-middle kernel only (P == 1, C == 64)
 };
 struct ScanWs {
   float* mat = nullptr;
@@ -151,6 +153,7 @@ size_t stream_ws(const ts_chain* c, const Plan& pl, bool marg, void* ws, StreamW
     w.alpha_hat = cv.take<float>((size_t)(B * N * C));
     w.mlag = cv.take<float>((size_t)(B * N));
     w.tmax = cv.take<float>((size_t)(B * (E > 0 ? E : 1)));
+    if (P == 1 && !force_tree && C == 64) w.beta_hat = cv.take<float>((size_t)(B * N * C));
   }
   w.alpha_end = cv.take<float>((size_t)(B * P * C));
   w.alpha_end_off = cv.take<double>((size_t)(B * P));
@@ -233,7 +236,15 @@ ts_status run_log(const ts_chain* c, float* marg, float* logz, uint32_t* flags, 
   ScanWs sw;
   const size_t need = stream_ws(c, p, marg != nullptr, ws, &w, &sw);
   if (ws_bytes < need || (need && (!ws || !aligned(ws, kAlign)))) return TS_E_WORKSPACE;
-  cudaError_t e = cudaMemsetAsync(w.wflags, 0, sizeof(uint32_t) * (size_t)c->B, st);
+  cudaError_t e;
+  if (marg && p.P == 1 && w.beta_hat && meet_ok(c->C, c->pot, marg) && g_meet.load()) {
+    MeetArgs m{c->pot, c->lengths, c->B, c->N, marg, logz, flags,
+               w.alpha_hat, w.beta_hat, w.mlag, w.tmax};
+    if ((e = launch_meet(m, c->C, st)) != cudaSuccess) return cuda_status(e);
+    t_launches = 1;
+    return TS_OK;
+  }
+  e = cudaMemsetAsync(w.wflags, 0, sizeof(uint32_t) * (size_t)c->B, st);
   if (e != cudaSuccess) return cuda_status(e);
   int n = 0;
   ScanArgs sa{};
@@ -571,6 +582,7 @@ TS_API ts_status ts_segment_finish(const ts_chain* local, int64_t edge_begin, in
   return TS_OK;
 }
 
+TS_API void ts_set_meet(int enable) { g_meet.store(enable ? 1 : 0); }
 TS_API void ts_set_plan_chunk(int64_t L) { g_plan_chunk.store(L < 0 ? 0 : L); }
 TS_API int64_t ts_get_plan_chunk(void) { return g_plan_chunk.load(); }
 TS_API void ts_set_small_cluster(int G) {

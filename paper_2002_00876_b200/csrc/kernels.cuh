@@ -66,6 +66,24 @@ bool stream2_ok(const SweepArgs& a);
 cudaError_t launch_fwd2(const SweepArgs& a, cudaStream_t st);
 cudaError_t launch_bwd2(const SweepArgs& a, cudaStream_t st);
 
+// ---- meet-in-the-middle fused forward/backward + marginals, one CTA per sequence
+// (fb_meet.cu): two 256-thread engines sweep from both ends at once, exchange their node
+// vectors through HBM/L2 at the midpoint and each finishes the other half with marginals.
+struct MeetArgs {
+  const float* pot;
+  const int32_t* lengths;
+  int64_t B, N;
+  float* marg;       // [B][N-1][C][C]
+  float* logz;       // [B]
+  uint32_t* flags;   // [B] or nullptr
+  float* alpha_hat;  // [B][N][C] forward node vectors, nodes 0..h (scratch)
+  float* beta_hat;   // [B][N][C] backward node vectors, nodes h..E_b (scratch)
+  float* mlag;       // [B][N]  forward lag bound per edge t < h (scratch)
+  float* tshift;     // [B][N-1] natural-unit shift used for edge t (scratch)
+};
+bool meet_ok(int64_t C, const float* pot, const float* marg);
+cudaError_t launch_meet(const MeetArgs& a, int64_t C, cudaStream_t st);
+
 // ---- time-chunked scan (scan.cu): leaf summaries, up-sweep tree, down-sweep ---------
 // Tree of one sequence: levels 0..H, level l holds Ppad >> l nodes (Ppad = 2^H >= P),
 // `nodes` = 2*Ppad - 1 node slots per sequence.  LogMat node: mat [C][C] log2 values +
