@@ -163,6 +163,12 @@ TS_API void ts_set_small_cluster(int G);
  * backward sweep kernels.  Results agree within the parity tolerances. */
 TS_API void ts_set_meet(int enable);
 
+/* Debug/testing knob (process-global) for the Viterbi forward with C in {128, 256}:
+ * 0 (default) = automatic cluster column split (the largest G in {1,2,4,8} with B*G CTAs
+ * fitting the SMs, C/G >= 32); G in {1,2,4,8} = forced cluster size; -1 = the
+ * one-CTA-per-sequence kernel used for every other C.  Results are bit-identical. */
+TS_API void ts_set_viterbi_split(int G);
+
 /* Number of kernel launches the most recent successful call on this host thread
  * enqueued (bench accounting). */
 TS_API int ts_last_launch_count(void);

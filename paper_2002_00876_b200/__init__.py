@@ -219,6 +219,11 @@ def set_meet(enable: bool) -> None:
     _lib.load().ts_set_meet(1 if enable else 0)
 
 
+def set_viterbi_split(G: int) -> None:
+    """Debug knob: Viterbi C in {128,256} cluster size (0 auto, 1/2/4/8 forced, -1 legacy)."""
+    _lib.load().ts_set_viterbi_split(int(G))
+
+
 def get_plan_chunk() -> int:
     return int(_lib.load().ts_get_plan_chunk())
 

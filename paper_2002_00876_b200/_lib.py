@@ -21,7 +21,7 @@ STATUS = {0: "TS_OK", 1: "TS_E_INVALID", 2: "TS_E_UNSUPPORTED", 3: "TS_E_WORKSPA
 SYMBOLS = ("ts_workspace_bytes", "ts_logpartition", "ts_marginals", "ts_viterbi",
            "ts_marginals_host", "ts_segment_summary_bytes", "ts_segment_summary",
            "ts_segment_finish", "ts_set_plan_chunk", "ts_get_plan_chunk", "ts_set_small_cluster",
-           "ts_set_meet",
+           "ts_set_meet", "ts_set_viterbi_split",
            "ts_last_launch_count", "ts_status_str", "ts_version")
 
 
@@ -71,6 +71,8 @@ def load():
     L.ts_set_small_cluster.restype = None
     L.ts_set_meet.argtypes = [INT]
     L.ts_set_meet.restype = None
+    L.ts_set_viterbi_split.argtypes = [INT]
+    L.ts_set_viterbi_split.restype = None
     L.ts_last_launch_count.restype = INT
     L.ts_status_str.argtypes = [INT]
     L.ts_status_str.restype = ctypes.c_char_p

@@ -15,7 +15,8 @@ namespace {
 
 std::atomic<int64_t> g_plan_chunk{0};
 std::atomic<int> g_small_cluster{0};
-std::atomic<int> g_meet{1};  // meet-in-the-middle marginals kernel for C = 64  // debug: run short C<=32 chains on G-CTA clusters
+std::atomic<int> g_meet{1};
+std::atomic<int> g_vsplit{0};  // Viterbi: -1 one CTA per sequence, 0 auto, G forced cluster size  // meet-in-the-middle marginals kernel for C = 64  // debug: run short C<=32 chains on G-CTA clusters
 thread_local int t_launches = 0;
 
 constexpr size_t kAlign = 256;
@@ -336,7 +337,7 @@ ts_status run_max(const ts_chain* c, int op, float* marg, float* logz, int32_t* 
   a.marg = marg;
   a.logz = logz;
   int n = 0;
-  ts_status r = cuda_status(launch_viterbi(a, st, &n));
+  ts_status r = cuda_status(launch_viterbi(a, st, &n, g_vsplit.load()));
   if (r == TS_OK) t_launches = n;
   return r;
 }
@@ -583,6 +584,9 @@ TS_API ts_status ts_segment_finish(const ts_chain* local, int64_t edge_begin, in
 }
 
 TS_API void ts_set_meet(int enable) { g_meet.store(enable ? 1 : 0); }
+TS_API void ts_set_viterbi_split(int G) {
+  g_vsplit.store((G == -1 || G == 1 || G == 2 || G == 4 || G == 8) ? G : 0);
+}
 TS_API void ts_set_plan_chunk(int64_t L) { g_plan_chunk.store(L < 0 ? 0 : L); }
 TS_API int64_t ts_get_plan_chunk(void) { return g_plan_chunk.load(); }
 TS_API void ts_set_small_cluster(int G) {

@@ -133,6 +133,11 @@ struct VitArgs {
   float* logz;      // [B] copy of the score for ts_logpartition/ts_marginals(TS_MAX), or nullptr
 };
 size_t vit_smem_bytes(int64_t C, int stages, int rows_per_stage);
-cudaError_t launch_viterbi(const VitArgs& a, cudaStream_t st, int* launches);
+// vsplit: -1 = one-CTA-per-sequence kernel for every C; 0 = auto (cluster column split for
+// C in {128, 256}); 1/2/4/8 = forced cluster size for C in {128, 256}.
+cudaError_t launch_viterbi(const VitArgs& a, cudaStream_t st, int* launches, int vsplit);
+// cluster column-split forward (viterbi2.cu)
+bool vit2_ok(const VitArgs& a);
+cudaError_t launch_vit2(const VitArgs& a, int g_force, cudaStream_t st);
 
 }  // namespace tsb

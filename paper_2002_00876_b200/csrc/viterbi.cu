@@ -221,6 +221,8 @@ __global__ void __launch_bounds__(256) indicator_kernel(VitArgs a) {
   for (int64_t q = threadIdx.x; q < CC; q += blockDim.x) m[q] = (q == hot) ? 1.f : 0.f;
 }
 
+cudaError_t launch_vit1(const VitArgs& a, cudaStream_t st);
+
 namespace {
 std::atomic<uint64_t> g_attr_vit{0};
 template <typename K>
@@ -235,7 +237,29 @@ cudaError_t set_smem(K kern, int bit) {
 }
 }  // namespace
 
-cudaError_t launch_viterbi(const VitArgs& a, cudaStream_t st, int* launches) {
+cudaError_t launch_viterbi(const VitArgs& a, cudaStream_t st, int* launches, int vsplit) {
+  cudaError_t e;
+  if (vsplit >= 0 && vit2_ok(a)) {
+    if ((e = launch_vit2(a, vsplit, st)) != cudaSuccess) return e;
+  } else {
+    if ((e = launch_vit1(a, st)) != cudaSuccess) return e;
+  }
+  int n = 1;
+  if (a.path) {
+    backtrack_kernel<<<(unsigned)a.B, 32, kBtRows * 256 + kBtRows * 4, st>>>(a);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    ++n;
+  }
+  if (a.marg && a.N > 1) {
+    indicator_kernel<<<dim3((unsigned)(a.N - 1), (unsigned)a.B), 256, 0, st>>>(a);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    ++n;
+  }
+  if (launches) *launches = n;
+  return cudaSuccess;
+}
+
+cudaError_t launch_vit1(const VitArgs& a, cudaStream_t st) {
   const int C = (int)a.C;
   const int RB = vit_rows(C);
   const size_t stage = (((size_t)RB * C) + 3) & ~(size_t)3;
@@ -251,20 +275,7 @@ cudaError_t launch_viterbi(const VitArgs& a, cudaStream_t st, int* launches) {
     if ((e = set_smem(viterbi_fwd_kernel<false>, 1)) != cudaSuccess) return e;
     viterbi_fwd_kernel<false><<<(unsigned)a.B, vit_threads(C), smem, st>>>(a, S, RB);
   }
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  int n = 1;
-  if (a.path) {
-    backtrack_kernel<<<(unsigned)a.B, 32, kBtRows * 256 + kBtRows * 4, st>>>(a);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    ++n;
-  }
-  if (a.marg && a.N > 1) {
-    indicator_kernel<<<dim3((unsigned)(a.N - 1), (unsigned)a.B), 256, 0, st>>>(a);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    ++n;
-  }
-  if (launches) *launches = n;
-  return cudaSuccess;
+  return cudaGetLastError();
 }
 
 }  // namespace tsb
