@@ -163,10 +163,13 @@ __global__ void __launch_bounds__(256) viterbi_fwd_kernel(VitArgs a, int S, int 
   }
 }
 
-// One warp per sequence: stage backpointer rows in SMEM (coalesced), walk back serially.
-constexpr int kBtRows = 64;
+// One warp per sequence: backpointer rows are staged in SMEM in chunks of kBtRows rows
+// (double-buffered 1-D bulk copies when C % 16 == 0, else a cooperative copy) while lane 0
+// walks the previous chunk back serially; the path is written with coalesced stores.
+constexpr int kBtRows = 128;
+constexpr size_t kBtSmem = 2 * kBtRows * 256 + kBtRows * 4 + 32;
 __global__ void __launch_bounds__(32) backtrack_kernel(VitArgs a) {
-  extern __shared__ __align__(16) uint8_t bsm[];
+  extern __shared__ __align__(128) uint8_t bsm[];
   const int C = (int)a.C;
   const int64_t N = a.N, E = N - 1;
   const int64_t b = blockIdx.x;
@@ -182,24 +185,51 @@ __global__ void __launch_bounds__(32) backtrack_kernel(VitArgs a) {
   const int64_t Eb = len - 1;
   if (pb)
     for (int64_t n = Eb + 1 + lane; n < N; n += 32) pb[n] = -1;
-  int32_t* zs = reinterpret_cast<int32_t*>(bsm + kBtRows * 256);
+  uint8_t* buf[2] = {bsm, bsm + kBtRows * 256};
+  int32_t* zs = reinterpret_cast<int32_t*>(bsm + 2 * kBtRows * 256);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(bsm + 2 * kBtRows * 256 + kBtRows * 4);
+  const uint8_t* bpb = a.bp + b * E * C;
+  const bool bulk = (C & 15) == 0 && ((reinterpret_cast<uintptr_t>(bpb)) & 15) == 0;
+  const int64_t nchunk = (Eb + kBtRows - 1) / kBtRows;  // chunk k: rows [lo_k, hi_k), from the top
+  auto lo_of = [&](int64_t k) { const int64_t hi = Eb - k * kBtRows; return hi - kBtRows > 0 ? hi - kBtRows : 0; };
+  auto hi_of = [&](int64_t k) { return Eb - k * kBtRows; };
+  if (bulk) {
+    if (lane == 0) {
+      mbar_init(&bar[0], 1);
+      mbar_init(&bar[1], 1);
+      fence_mbar_init();
+      for (int64_t k = 0; k < 2 && k < nchunk; ++k) {
+        const int64_t lo = lo_of(k), n = hi_of(k) - lo;
+        bulk_load(buf[k & 1], bpb + lo * C, (uint32_t)(n * C), &bar[k & 1]);
+      }
+    }
+    __syncwarp();
+  }
   int z = z_end;
   if (lane == 0 && pb) pb[Eb] = z;
-  const uint8_t* bpb = a.bp + b * E * C;
-  for (int64_t hi = Eb; hi > 0; hi -= kBtRows) {
-    const int64_t lo = hi - kBtRows > 0 ? hi - kBtRows : 0;  // rows [lo, hi)
+  for (int64_t k = 0; k < nchunk; ++k) {
+    const int64_t lo = lo_of(k), hi = hi_of(k);
     const int nrow = (int)(hi - lo);
-    const int nbytes = nrow * C;
-    const uint8_t* src = bpb + lo * C;
-    for (int q = lane; q < nbytes; q += 32) bsm[q] = src[q];
-    __syncwarp();
+    uint8_t* rows = buf[k & 1];
+    if (bulk) {
+      mbar_wait(&bar[k & 1], (uint32_t)((k >> 1) & 1));
+    } else {
+      const uint8_t* src = bpb + lo * C;
+      for (int q = lane; q < nrow * C; q += 32) rows[q] = src[q];
+      __syncwarp();
+    }
     if (lane == 0) {
       for (int r = nrow - 1; r >= 0; --r) {
-        z = bsm[r * C + z];
+        z = rows[r * C + z];
         zs[r] = z;
       }
     }
     __syncwarp();
+    if (bulk && lane == 0 && k + 2 < nchunk) {  // refill this buffer with chunk k+2
+      const int64_t lo2 = lo_of(k + 2), n2 = hi_of(k + 2) - lo2;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads before async writes
+      bulk_load(rows, bpb + lo2 * C, (uint32_t)(n2 * C), &bar[k & 1]);
+    }
     z = __shfl_sync(0xffffffffu, z, 0);
     if (pb)
       for (int r = lane; r < nrow; r += 32) pb[lo + r] = zs[r];
@@ -246,7 +276,8 @@ cudaError_t launch_viterbi(const VitArgs& a, cudaStream_t st, int* launches, int
   }
   int n = 1;
   if (a.path) {
-    backtrack_kernel<<<(unsigned)a.B, 32, kBtRows * 256 + kBtRows * 4, st>>>(a);
+    if ((e = set_smem(backtrack_kernel, 2)) != cudaSuccess) return e;
+    backtrack_kernel<<<(unsigned)a.B, 32, kBtSmem, st>>>(a);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     ++n;
   }
