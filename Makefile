@@ -22,7 +22,7 @@ build/%.o: $(CSRC)/%.cu $(KERN_HDRS)
 	$(NVCC) $(NVFLAGS) -Iinclude -c -o $@ $<
 
 $(PKG)/libts_b200.so: $(KERN_OBJS)
-	$(NVCC) $(NVFLAGS) -shared -o $@ $(KERN_OBJS) -lcuda
+	$(NVCC) $(NVFLAGS) -shared -o $@ $(KERN_OBJS)
 
 tsgen/libtsgen_device.so: tsgen/tsgen_device.cu tsgen/tsgen.h
 	$(NVCC) $(NVFLAGS) -shared -o $@ tsgen/tsgen_device.cu

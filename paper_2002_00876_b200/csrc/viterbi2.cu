@@ -279,6 +279,21 @@ __global__ void __launch_bounds__(kVT + 32, 1) vit2_kernel(VitArgs a, const __gr
 
 std::atomic<uint64_t> g_vit2_attr{0};
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point: the library then has no
+// link-time dependency on libcuda.so (it loads on hosts without a driver; the CPU ABI tests).
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+PFN_encodeTiled resolve_encode_tiled() {
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess)
+    return nullptr;
+  return reinterpret_cast<PFN_encodeTiled>(fn);
+}
+
 template <int C, int G>
 cudaError_t launch_cg(const VitArgs& a, cudaStream_t st, int bit) {
   using L = VL<C, G>;
@@ -301,7 +316,9 @@ cudaError_t launch_cg(const VitArgs& a, cudaStream_t st, int bit) {
     const cuuint64_t strides[1] = {(cuuint64_t)C * 4};
     const cuuint32_t box[2] = {(cuuint32_t)L::CP, (cuuint32_t)kRB};
     const cuuint32_t estr[2] = {1, 1};
-    if (cuTensorMapEncodeTiled(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(a.pot), dims,
+    static PFN_encodeTiled encode = resolve_encode_tiled();
+    if (!encode) return cudaErrorNotSupported;
+    if (encode(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(a.pot), dims,
                                strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                                CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
