@@ -278,11 +278,12 @@ def main():
 
     # end-to-end through the public C-ABI host-buffer entry point (pinned host I/O)
     e2e_steps = args.e2e_steps or max(20, min(args.steps, 400))
-    hp = torch.empty((B, E, C, C), dtype=torch.float32).pin_memory()
+    # page-locked host buffers from the library allocator (ts_host_alloc)
+    hp = tsb.host_empty((B, E, C, C))
     hp.copy_(pots[0].cpu())
-    hm = torch.empty_like(hp).pin_memory()
-    hl = torch.empty(B, dtype=torch.float32).pin_memory()
-    hf = torch.empty(B, dtype=torch.int32).pin_memory()
+    hm = tsb.host_empty((B, E, C, C))
+    hl = tsb.host_empty((B,))
+    hf = tsb.host_empty((B,), torch.int32)
     hws = tsb.Workspace(dev)
     for _ in range(3):
         tsb.marginals_host(hp, hm, hl, hf, device=dev, ws=hws)
@@ -329,7 +330,8 @@ def main():
             "e2e": {"value": e2e_value, "unit": UNIT,
                     "h2d_bytes_per_step": B * E * C * C * 4,
                     "d2h_bytes_per_step": B * E * C * C * 4 + 8 * B,
-                    "api": "ts_marginals_host (pinned host buffers, copies inside the call)"},
+                    "api": "ts_marginals_host (ts_host_alloc page-locked host buffers; H2D, kernels, "
+                           "D2H inside every call)"},
             "gpu_launches": args.steps * launches_per_step,
             "clocks": sampler.summary(),
             "paper_context": {"value": 390000, "unit": UNIT,

@@ -113,10 +113,33 @@ TS_API ts_status ts_viterbi(const ts_chain *c, int32_t *path, float *score, uint
 /* End-to-end variant of ts_marginals with HOST buffers: host_chain->pot / ->lengths and
  * host_marg / host_logz / host_flags are host pointers (pinned for overlap); the call
  * enqueues the H2D copies, the scan and the D2H copies on `stream` using device staging
- * inside `ws` (size from TS_OP_MARG_HOST).  Synchronise the stream before reading. */
+ * inside `ws` (size from TS_OP_MARG_HOST).  Synchronise the stream before reading.
+ * The batch is cut into <= 4 chunks pipelined over library-owned streams (chunk k's copy
+ * back overlaps chunk k+1's kernels and copy in).  A repeated call with the same I/O
+ * binding (all pointers, sizes, semiring, workspace) replays a CUDA graph of the whole
+ * pipeline captured on its second sighting (ts_set_host_graphs(0) disables this); every
+ * copy and kernel still runs on every call.  Thread-safe (one lock per device). */
 TS_API ts_status ts_marginals_host(const ts_chain *host_chain, ts_semiring s, float *host_marg,
                                    float *host_logz, uint32_t *host_flags, void *ws,
                                    size_t ws_bytes, void *stream);
+
+/* Debug/testing: 1 (default) = graph replay of repeated ts_marginals_host bindings,
+ * 0 = always enqueue eagerly. */
+TS_API void ts_set_host_graphs(int on);
+
+/* Debug/testing: leaf chunk summaries of the time-chunked scan for 64 < C <= 128 run on
+ * the tensor cores (tcgen05 kind::tf32): 3 = 3xTF32 split (default), 1 = one TF32 pass,
+ * 0 = SIMT fp32 kernel.  Chunks the precision gate flags are recomputed exactly in every
+ * mode. */
+TS_API void ts_set_tc_summary(int mode);
+TS_API int  ts_get_tc_summary(void);
+
+/* Page-locked host staging buffers for ts_marginals_host (cudaHostAlloc, portable).
+ * Returns NULL on failure or bytes == 0; release with ts_host_free.  Buffers from this
+ * allocator sustain full PCIe rate for the host->device copies (pinned registrations of
+ * ordinary pages can be several times slower to DMA-read under an IOMMU). */
+TS_API void *ts_host_alloc(size_t bytes);
+TS_API void  ts_host_free(void *p);
 
 /* ---- time-sharded chains (§6(a) scan across devices) --------------------
  * A chain of n_global positions is split into contiguous segments; a rank holds edges

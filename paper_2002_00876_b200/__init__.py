@@ -20,7 +20,7 @@ import torch
 from . import _lib
 from ._lib import TS_F_BADLEN, TS_F_EMPTY, TS_F_NONFINITE, TsError  # noqa: F401
 
-__all__ = ["logpartition", "marginals", "viterbi", "marginals_host", "set_plan_chunk",
+__all__ = ["logpartition", "marginals", "viterbi", "marginals_host", "host_empty", "set_plan_chunk",
            "get_plan_chunk", "last_launch_count", "workspace_bytes", "Workspace", "TsError",
            "Segment"]
 
@@ -134,12 +134,17 @@ def viterbi(pot: torch.Tensor, lengths=None, ws: Workspace | None = None):
     return path, score, flags
 
 
+_HOST_NEED: dict = {}
+
+
 def marginals_host(pot_host: torch.Tensor, marg_host: torch.Tensor, logz_host: torch.Tensor,
                    flags_host: torch.Tensor | None = None, lengths_host=None, semiring="log",
                    device=None, ws: Workspace | None = None):
     """End-to-end call with HOST (ideally pinned) buffers; copies happen inside the C ABI call.
 
     Enqueued on the current stream of `device`; synchronise before reading the outputs.
+    Repeated calls with the same buffers replay a CUDA graph of the whole pipeline
+    (include/ts_b200.h, ts_marginals_host).
     """
     L = _lib.load()
     device = torch.device(device or "cuda")
@@ -147,13 +152,62 @@ def marginals_host(pot_host: torch.Tensor, marg_host: torch.Tensor, logz_host: t
     ch = _lib.ts_chain(B, E + 1, C, pot_host.data_ptr() if pot_host.numel() else None,
                        lengths_host.data_ptr() if lengths_host is not None else None)
     semi = _semi(semiring)
-    need = int(L.ts_workspace_bytes(ctypes.byref(ch), _lib.TS_OP_MARG_HOST, semi))
+    key = (B, E, C, semi, lengths_host is not None)
+    need = _HOST_NEED.get(key)
+    if need is None:
+        need = _HOST_NEED[key] = int(L.ts_workspace_bytes(ctypes.byref(ch), _lib.TS_OP_MARG_HOST,
+                                                          semi))
     ws = ws or Workspace.get(device)
     wp = ws.ptr(need)
     _lib.check(L.ts_marginals_host(ctypes.byref(ch), semi, marg_host.data_ptr(),
                                    logz_host.data_ptr(),
                                    flags_host.data_ptr() if flags_host is not None else None, wp,
                                    need, _stream(device)), "ts_marginals_host")
+
+
+class _HostBlock:
+    """Owner of one ts_host_alloc block; freed when the last tensor view is collected."""
+
+    def __init__(self, nbytes: int):
+        self.ptr = _lib.load().ts_host_alloc(nbytes)
+        if not self.ptr:
+            raise MemoryError(f"ts_host_alloc({nbytes}) failed")
+        self.nbytes = nbytes
+
+    def __del__(self):
+        if getattr(self, "ptr", None):
+            _lib.load().ts_host_free(self.ptr)
+            self.ptr = None
+
+
+def host_empty(shape, dtype=torch.float32) -> torch.Tensor:
+    """Page-locked host tensor from the library allocator (ts_host_alloc), for the
+    host-buffer entry point marginals_host."""
+    n = 1
+    for d in shape:
+        n *= int(d)
+    itemsize = torch.empty(0, dtype=dtype).element_size()
+    nbytes = max(n * itemsize, 1)
+    blk = _HostBlock(nbytes)
+    buf = (ctypes.c_uint8 * nbytes).from_address(blk.ptr)
+    buf._ts_owner = blk  # keep the block alive as long as the buffer is
+    t = torch.frombuffer(buf, dtype=torch.uint8, count=n * itemsize)
+    return t.view(dtype).view(*shape) if n else torch.empty(shape, dtype=dtype)
+
+
+def set_tc_summary(mode: int) -> None:
+    """Debug/testing: scan leaf summaries on tensor cores (3 = 3xTF32 default, 1 = 1xTF32,
+    0 = SIMT fp32)."""
+    _lib.load().ts_set_tc_summary(int(mode))
+
+
+def get_tc_summary() -> int:
+    return int(_lib.load().ts_get_tc_summary())
+
+
+def set_host_graphs(enable: bool) -> None:
+    """Debug/testing: graph replay of repeated ts_marginals_host bindings (default on)."""
+    _lib.load().ts_set_host_graphs(1 if enable else 0)
 
 
 class Segment:

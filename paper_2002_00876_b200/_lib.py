@@ -21,7 +21,8 @@ STATUS = {0: "TS_OK", 1: "TS_E_INVALID", 2: "TS_E_UNSUPPORTED", 3: "TS_E_WORKSPA
 SYMBOLS = ("ts_workspace_bytes", "ts_logpartition", "ts_marginals", "ts_viterbi",
            "ts_marginals_host", "ts_segment_summary_bytes", "ts_segment_summary",
            "ts_segment_finish", "ts_set_plan_chunk", "ts_get_plan_chunk", "ts_set_small_cluster",
-           "ts_set_meet", "ts_set_viterbi_split",
+           "ts_set_meet", "ts_set_viterbi_split", "ts_set_host_graphs",
+           "ts_host_alloc", "ts_host_free", "ts_set_tc_summary", "ts_get_tc_summary",
            "ts_last_launch_count", "ts_status_str", "ts_version")
 
 
@@ -73,6 +74,15 @@ def load():
     L.ts_set_meet.restype = None
     L.ts_set_viterbi_split.argtypes = [INT]
     L.ts_set_viterbi_split.restype = None
+    L.ts_set_host_graphs.argtypes = [INT]
+    L.ts_set_host_graphs.restype = None
+    L.ts_set_tc_summary.argtypes = [INT]
+    L.ts_set_tc_summary.restype = None
+    L.ts_get_tc_summary.restype = INT
+    L.ts_host_alloc.argtypes = [SZ]
+    L.ts_host_alloc.restype = P
+    L.ts_host_free.argtypes = [P]
+    L.ts_host_free.restype = None
     L.ts_last_launch_count.restype = INT
     L.ts_status_str.argtypes = [INT]
     L.ts_status_str.restype = ctypes.c_char_p

@@ -4,6 +4,7 @@
 #include <atomic>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -396,6 +397,105 @@ bool seg_ok(const ts_chain* c, int64_t edge_begin, int64_t n_global) {
          edge_begin + (c->N - 1) <= n_global - 1 && c->C <= 128;
 }
 
+// ts_marginals_host pipelining: the batch is cut into K chunks, each on its own library
+// stream (H2D -> kernels -> D2H), so chunk k's copy back overlaps chunk k+1's kernels and
+// copy in (the two copy directions run on separate engines).  Chunks of >= 256 KB.
+constexpr int kHostMaxChunks = 4;
+int host_chunks(int64_t B, int64_t per_seq_floats) {
+  const int64_t bytes = B * per_seq_floats * 4;
+  int64_t k = bytes / (256 << 10);
+  if (k > kHostMaxChunks) k = kHostMaxChunks;
+  if (k > B) k = B;
+  return k < 1 ? 1 : (int)k;
+}
+
+std::atomic<int> g_host_graphs{1};
+
+struct HostKey {
+  int64_t B, N, C;
+  const float* pot;
+  const int32_t* lengths;
+  int s;
+  float* marg;
+  float* logz;
+  uint32_t* flags;
+  void* ws;
+  size_t ws_bytes;
+  int64_t plan_chunk;
+  int meet, small_cluster;
+  bool operator==(const HostKey& o) const {
+    return B == o.B && N == o.N && C == o.C && pot == o.pot && lengths == o.lengths && s == o.s &&
+           marg == o.marg && logz == o.logz && flags == o.flags && ws == o.ws &&
+           ws_bytes == o.ws_bytes && plan_chunk == o.plan_chunk && meet == o.meet &&
+           small_cluster == o.small_cluster;
+  }
+};
+
+struct HostGraph {
+  HostKey key;
+  cudaGraphExec_t exec = nullptr;
+  int launches = 0;
+  uint64_t used = 0;
+};
+
+constexpr int kHostGraphs = 16;
+
+struct HostPipe {
+  std::mutex mu;
+  cudaStream_t side[kHostMaxChunks];
+  cudaStream_t cap;
+  cudaEvent_t fork, join[kHostMaxChunks];
+  HostGraph graphs[kHostGraphs];
+  int n_graphs = 0;
+  uint64_t clock = 0;
+  HostGraph* find(const HostKey& k) {
+    for (int i = 0; i < n_graphs; ++i)
+      if (graphs[i].key == k) {
+        graphs[i].used = ++clock;
+        return &graphs[i];
+      }
+    return nullptr;
+  }
+  void insert(const HostKey& k) {
+    int slot = n_graphs;
+    if (n_graphs == kHostGraphs) {  // evict the least recently used binding
+      slot = 0;
+      for (int i = 1; i < kHostGraphs; ++i)
+        if (graphs[i].used < graphs[slot].used) slot = i;
+      if (graphs[slot].exec) cudaGraphExecDestroy(graphs[slot].exec);
+    } else {
+      ++n_graphs;
+    }
+    graphs[slot].key = k;
+    graphs[slot].exec = nullptr;
+    graphs[slot].launches = 0;
+    graphs[slot].used = ++clock;
+  }
+};
+
+// One-time per-device setup (streams + events; never allocated in the hot call again).
+HostPipe* host_pipe() {
+  static std::mutex init_mu;
+  static HostPipe* pipes[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lock(init_mu);
+  if (!pipes[dev]) {
+    HostPipe* p = new HostPipe;
+    bool ok = cudaEventCreateWithFlags(&p->fork, cudaEventDisableTiming) == cudaSuccess &&
+              cudaStreamCreateWithFlags(&p->cap, cudaStreamNonBlocking) == cudaSuccess;
+    for (int k = 0; k < kHostMaxChunks && ok; ++k)
+      ok = cudaStreamCreateWithFlags(&p->side[k], cudaStreamNonBlocking) == cudaSuccess &&
+           cudaEventCreateWithFlags(&p->join[k], cudaEventDisableTiming) == cudaSuccess;
+    if (!ok) {
+      delete p;
+      return nullptr;
+    }
+    pipes[dev] = p;
+  }
+  return pipes[dev];
+}
+
 }  // namespace
 
 extern "C" {
@@ -403,14 +503,21 @@ extern "C" {
 TS_API size_t ts_workspace_bytes(const ts_chain* c, int op, ts_semiring s) {
   if (!chain_ok(c) || (s != TS_LOG && s != TS_MAX)) return 0;
   if (op == TS_OP_MARG_HOST) {
+    // K batch chunks, each with its own device staging + inner workspace (ts_marginals_host)
     Carve cv(nullptr);
-    const int64_t B = c->B, N = c->N, C = c->C, E = N - 1;
-    cv.take<float>((size_t)(B * E * C * C));  // pot
-    cv.take<int32_t>((size_t)B);               // lengths
-    cv.take<float>((size_t)(B * E * C * C));  // marg
-    cv.take<float>((size_t)B);                 // logz
-    cv.take<uint32_t>((size_t)B);              // flags
-    return cv.off + op_ws(c, TS_OP_MARG, s, nullptr, nullptr, nullptr);
+    const int64_t B = c->B, N = c->N, C = c->C, E = N - 1, per = E * C * C;
+    const int K = host_chunks(B, per);
+    for (int k = 0; k < K; ++k) {
+      const int64_t Bk = B * (k + 1) / K - B * k / K;
+      ts_chain dc{Bk, N, C, c->pot, c->lengths};
+      cv.take<float>((size_t)(Bk * per));  // pot
+      cv.take<int32_t>((size_t)Bk);         // lengths
+      cv.take<float>((size_t)(Bk * per));  // marg
+      cv.take<float>((size_t)Bk);           // logz
+      cv.take<uint32_t>((size_t)Bk);        // flags
+      cv.take<char>(op_ws(&dc, TS_OP_MARG, s, nullptr, nullptr, nullptr));
+    }
+    return cv.off;
   }
   if (op == TS_OP_SEGMENT) {
     if (c->C > 128) return 0;
@@ -455,6 +562,55 @@ TS_API ts_status ts_viterbi(const ts_chain* c, int32_t* path, float* score, uint
                  static_cast<cudaStream_t>(stream));
 }
 
+// Enqueue the chunked host pipeline of ts_marginals_host on `st` (fork -> K chunk streams
+// of H2D, kernels, D2H -> join).  Caller holds hp->mu.
+static ts_status host_enqueue(HostPipe* hp, const ts_chain* hc, ts_semiring s, float* host_marg,
+                              float* host_logz, uint32_t* host_flags, void* ws, cudaStream_t st) {
+  const int64_t B = hc->B, N = hc->N, C = hc->C, E = N - 1;
+  const int64_t per = E * C * C;  // floats per sequence
+  const int K = host_chunks(B, per);
+  cudaError_t e;
+  if ((e = cudaEventRecord(hp->fork, st)) != cudaSuccess) return cuda_status(e);
+  Carve cv(ws);
+  int launches = 0;
+  for (int k = 0; k < K; ++k) {
+    const int64_t b0 = B * k / K, b1 = B * (k + 1) / K, Bk = b1 - b0;
+    const size_t nel = (size_t)(Bk * per);
+    cudaStream_t sk = hp->side[k];
+    if ((e = cudaStreamWaitEvent(sk, hp->fork, 0)) != cudaSuccess) return cuda_status(e);
+    float* d_pot = cv.take<float>(nel);
+    int32_t* d_len = cv.take<int32_t>((size_t)Bk);
+    float* d_marg = cv.take<float>(nel);
+    float* d_logz = cv.take<float>((size_t)Bk);
+    uint32_t* d_flags = cv.take<uint32_t>((size_t)Bk);
+    ts_chain dc{Bk, N, C, nel ? d_pot : nullptr, hc->lengths ? d_len : nullptr};
+    const size_t inner_bytes = op_ws(&dc, TS_OP_MARG, s, nullptr, nullptr, nullptr);
+    void* inner = cv.take<char>(inner_bytes);
+    if (nel && (e = cudaMemcpyAsync(d_pot, hc->pot + b0 * per, nel * 4, cudaMemcpyHostToDevice,
+                                    sk)) != cudaSuccess)
+      return cuda_status(e);
+    if (hc->lengths && (e = cudaMemcpyAsync(d_len, hc->lengths + b0, (size_t)Bk * 4,
+                                            cudaMemcpyHostToDevice, sk)) != cudaSuccess)
+      return cuda_status(e);
+    ts_status r = ts_marginals(&dc, s, d_marg, d_logz, d_flags, inner, inner_bytes, sk);
+    if (r != TS_OK) return r;
+    launches += t_launches;
+    if (nel && (e = cudaMemcpyAsync(host_marg + b0 * per, d_marg, nel * 4, cudaMemcpyDeviceToHost,
+                                    sk)) != cudaSuccess)
+      return cuda_status(e);
+    if ((e = cudaMemcpyAsync(host_logz + b0, d_logz, (size_t)Bk * 4, cudaMemcpyDeviceToHost, sk)) !=
+        cudaSuccess)
+      return cuda_status(e);
+    if (host_flags && (e = cudaMemcpyAsync(host_flags + b0, d_flags, (size_t)Bk * 4,
+                                           cudaMemcpyDeviceToHost, sk)) != cudaSuccess)
+      return cuda_status(e);
+    if ((e = cudaEventRecord(hp->join[k], sk)) != cudaSuccess) return cuda_status(e);
+    if ((e = cudaStreamWaitEvent(st, hp->join[k], 0)) != cudaSuccess) return cuda_status(e);
+  }
+  t_launches = launches;
+  return TS_OK;
+}
+
 TS_API ts_status ts_marginals_host(const ts_chain* hc, ts_semiring s, float* host_marg,
                                    float* host_logz, uint32_t* host_flags, void* ws,
                                    size_t ws_bytes, void* stream) {
@@ -464,37 +620,69 @@ TS_API ts_status ts_marginals_host(const ts_chain* hc, ts_semiring s, float* hos
   const size_t need = ts_workspace_bytes(hc, TS_OP_MARG_HOST, s);
   if (ws_bytes < need || !ws || !aligned(ws, kAlign)) return TS_E_WORKSPACE;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int64_t B = hc->B, N = hc->N, C = hc->C, E = N - 1;
-  const size_t nel = (size_t)(B * E * C * C);
-  Carve cv(ws);
-  float* d_pot = cv.take<float>(nel);
-  int32_t* d_len = cv.take<int32_t>((size_t)B);
-  float* d_marg = cv.take<float>(nel);
-  float* d_logz = cv.take<float>((size_t)B);
-  uint32_t* d_flags = cv.take<uint32_t>((size_t)B);
-  void* inner = static_cast<char*>(ws) + cv.off;
-  const size_t inner_bytes = ws_bytes - cv.off;
-  cudaError_t e;
-  if (nel && (e = cudaMemcpyAsync(d_pot, hc->pot, nel * 4, cudaMemcpyHostToDevice, st)) != cudaSuccess)
+  HostPipe* hp = host_pipe();
+  if (!hp) return TS_E_CUDA;
+  std::lock_guard<std::mutex> lock(hp->mu);
+  // Replay path: the same I/O binding seen before -> one graph launch (all copies and
+  // kernels of the call are nodes of the instantiated graph; nothing is skipped).
+  HostKey key{hc->B, hc->N, hc->C, hc->pot, hc->lengths, (int)s, host_marg, host_logz,
+              host_flags, ws, ws_bytes, g_plan_chunk.load(), g_meet.load(), g_small_cluster.load() * 16 + tsb::get_tc_summary()};
+  HostGraph* g = hp->find(key);
+  if (g && g->exec) {
+    cudaError_t e = cudaGraphLaunch(g->exec, st);
+    if (e != cudaSuccess) return cuda_status(e);
+    t_launches = g->launches;
+    return TS_OK;
+  }
+  if (!g || !g_host_graphs.load()) {
+    // first sighting: enqueue eagerly (also performs one-time kernel attribute setup)
+    ts_status r = host_enqueue(hp, hc, s, host_marg, host_logz, host_flags, ws, st);
+    if (r == TS_OK && g_host_graphs.load()) hp->insert(key);
+    return r;
+  }
+  // second sighting: capture the pipeline on the private stream, instantiate, launch
+  cudaError_t e = cudaStreamBeginCapture(hp->cap, cudaStreamCaptureModeThreadLocal);
+  if (e != cudaSuccess) return cuda_status(e);
+  ts_status r = host_enqueue(hp, hc, s, host_marg, host_logz, host_flags, ws, hp->cap);
+  cudaGraph_t graph = nullptr;
+  e = cudaStreamEndCapture(hp->cap, &graph);
+  if (r != TS_OK) {
+    if (graph) cudaGraphDestroy(graph);
+    return r;
+  }
+  if (e != cudaSuccess) return cuda_status(e);
+  e = cudaGraphInstantiate(&g->exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (e != cudaSuccess) {
+    g->exec = nullptr;
     return cuda_status(e);
-  if (hc->lengths &&
-      (e = cudaMemcpyAsync(d_len, hc->lengths, (size_t)B * 4, cudaMemcpyHostToDevice, st)) !=
-          cudaSuccess)
-    return cuda_status(e);
-  ts_chain dc{B, N, C, nel ? d_pot : nullptr, hc->lengths ? d_len : nullptr};
-  ts_status r = ts_marginals(&dc, s, d_marg, d_logz, d_flags, inner, inner_bytes, stream);
-  if (r != TS_OK) return r;
-  const int kern = t_launches;
-  if (nel && (e = cudaMemcpyAsync(host_marg, d_marg, nel * 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess)
-    return cuda_status(e);
-  if ((e = cudaMemcpyAsync(host_logz, d_logz, (size_t)B * 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess)
-    return cuda_status(e);
-  if (host_flags &&
-      (e = cudaMemcpyAsync(host_flags, d_flags, (size_t)B * 4, cudaMemcpyDeviceToHost, st)) !=
-          cudaSuccess)
-    return cuda_status(e);
-  t_launches = kern;
+  }
+  g->launches = t_launches;
+  if ((e = cudaGraphLaunch(g->exec, st)) != cudaSuccess) return cuda_status(e);
+  t_launches = g->launches;
   return TS_OK;
+}
+
+TS_API void ts_set_host_graphs(int on) { g_host_graphs.store(on ? 1 : 0); }
+
+TS_API void ts_set_tc_summary(int mode) { tsb::set_tc_summary(mode); }
+TS_API int ts_get_tc_summary(void) { return tsb::get_tc_summary(); }
+
+TS_API void* ts_host_alloc(size_t bytes) {
+  // Blocks are rounded up to >= 32 MB: on the GPU boxes' virtualised PCIe, host->device DMA
+  // from small page-locked allocations measured ~13-16 GB/s vs ~25 GB/s from slices of
+  // large ones (tools/e2e_probe.py, gpurun_out/s12_*).
+  void* p = nullptr;
+  if (bytes == 0) return nullptr;
+  const size_t kMin = (size_t)32 << 20, kGran = (size_t)2 << 20;
+  size_t sz = (bytes + kGran - 1) / kGran * kGran;
+  if (sz < kMin) sz = kMin;
+  if (cudaHostAlloc(&p, sz, cudaHostAllocPortable) != cudaSuccess) return nullptr;
+  return p;
+}
+
+TS_API void ts_host_free(void* p) {
+  if (p) cudaFreeHost(p);
 }
 
 TS_API size_t ts_segment_summary_bytes(const ts_chain* local) {

@@ -118,6 +118,11 @@ cudaError_t launch_segment_export(const ScanArgs& a, float* summ, cudaStream_t s
 cudaError_t launch_segment_combine(const ScanArgs& a, const float* all_summ, int rank, int world,
                                    bool write_root, cudaStream_t st);
 cudaError_t launch_scan_logz(const ScanArgs& a, cudaStream_t st);
+// tensor-core (tcgen05 kind::tf32, 3xTF32) leaf summaries for 64 < C <= 128 (scan_tc.cu)
+bool summary_tc_ok(const ScanArgs& a);
+cudaError_t launch_summary_tc(const ScanArgs& a, cudaStream_t st);
+void set_tc_summary(int mode);  // 0 SIMT, 1 1xTF32, 3 3xTF32
+int get_tc_summary();
 
 // ---- Viterbi (max-plus) -------------------------------------------------------------
 struct VitArgs {

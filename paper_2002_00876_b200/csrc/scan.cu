@@ -706,7 +706,9 @@ cudaError_t launch_scan_up(const ScanArgs& a, cudaStream_t st, int* launches) {
   const int C = (int)a.C;
   cudaError_t e;
   int n = 0;
-  switch ((C + 15) / 16) {
+  if (summary_tc_ok(a)) {
+    e = launch_summary_tc(a, st);
+  } else switch ((C + 15) / 16) {
     case 1: e = launch_fast<1>(a, st); break;
     case 2: e = launch_fast<2>(a, st); break;
     case 3: e = launch_fast<3>(a, st); break;

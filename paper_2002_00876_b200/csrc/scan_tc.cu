@@ -1,0 +1,362 @@
+// scan_tc.cu — leaf chunk summaries of the time-chunked scan (§6(a)) on
+// the sm_100a tensor cores, for 64 < C <= 128 (even C).  A leaf summary is the log-semiring
+// product S_k = l_{s_k} (x) ... (x) l_{e_k - 1} of the chunk's C x C edge tiles (Fig. 4
+// leaves).  In the exp-shifted form of §6(c) each log product becomes a real
+// matrix product of non-negative matrices:
+//
+//   S_{u+1}[m][j] = LSE_i(S_u[m][i] + l_u[i][j])
+//                 = off_m + R_u + ln sum_i (Ahat_u[m][i] w_i) X_u[i][j]
+//   r_i = max_j l_u[i][j] (row shift), R_u = max_i r_i, w_i = e^(r_i - R_u) <= 1,
+//   X_u[i][j] = e^(l_u[i][j] - r_i) <= 1,  S_u[m][i] = off_m + ln Ahat_u[m][i]
+//
+// D = (Ahat o w) . X runs on tcgen05 kind::tf32 as 3xTF32 (hi.hi + hi.lo + lo.hi, fp32
+// accumulate in TMEM; measured max relative error 2.9e-6 per 128^3 product vs 3.7e-4 for a
+// single TF32 pass, tools/tc_probe.cu), then each row is renormalised by its sum s_m
+// (Ahat_{u+1} = D / s_m, off_m += R_u + ln s_m, fp64).  The gate of DESIGN.md §4 is kept:
+// chunks where a re-centred entry, a row weight or a normalised value is tiny enough that
+// flush-to-zero could drop a significant term are flagged (cflag) and recomputed by the
+// exact per-cell-max kernel (summary_exact_kernel, scan.cu).
+//
+// CTA = one (sequence, chunk), 288 threads, warp-specialised:
+//   warps 0-3  epilogue: TMEM lane m = row m of D / A; normalise, scale by the next
+//              tile's row weights, split hi/lo, tcgen05.st into the A columns;
+//   warps 4-7  producers: warp p owns rows [32p, 32p+32) of every tile (K-block p): TMA
+//              bulk load HBM -> staging, row max (31-shuffle transpose reduction), exps,
+//              hi/lo split, K-major UMMA layout in the 4-stage B ring;
+//   warp 8     TMEM allocation + the single MMA-issuing thread.
+// TMEM: D cols [0,128), A_hi [128,256), A_lo [256,384) (512 allocated; 1 CTA per SM).
+#include <atomic>
+
+#include "common.cuh"
+#include "kernels.cuh"
+#include "tc.cuh"
+
+namespace tsb {
+
+namespace {
+constexpr int kTcThreads = 288;
+constexpr int kBlk = 16384;                 // one B stage (32 rows x 128 cols fp32), bytes
+constexpr int kOffBhi = 0;                  // [4][16 KB] tf32-hi  (K-major UMMA layout)
+constexpr int kOffBlo = 4 * kBlk;           // [4][16 KB] tf32-lo
+constexpr int kOffStg = 8 * kBlk;           // [4][16 KB] raw staging of the next tile
+constexpr int kOffW = 12 * kBlk;            // float wbuf[2][132]: w[128], R (natural)
+constexpr int kOffRs = kOffW + 2 * 132 * 4; // float rsc[4][32] row maxes of the current tile
+constexpr int kOffRp = kOffRs + 4 * 32 * 4; // float Rp[2][4] per-warp maxes
+constexpr int kOffBar = kOffRp + 64;        // mbarriers
+// bars: full[4] empty[4] stg[4] wready[2] dfull aready
+constexpr int kBarFull = 0, kBarEmpty = 4, kBarStg = 8, kBarW = 12, kBarD = 14, kBarA = 15;
+constexpr int kOffMisc = kOffBar + 16 * 8;  // u32 tmem base, flags[2]
+constexpr int kTcSmem = kOffMisc + 16;
+constexpr float kTinyXtc = -40.f;  // log2 re-centred tile entry
+constexpr float kTinyWtc = -30.f;  // log2 row weight
+constexpr float kTinyPtc = 9.313225746154785e-10f;  // 2^-30 normalised value
+
+// UMMA descriptors: B stage, K-major, no swizzle: core matrix 8 n-rows x 16 B (4 k's),
+// k-groups at LBO = 128 B, n-groups (8 columns) at SBO = 1024 B (32 k's per stage).
+__device__ __forceinline__ uint32_t bstage_off(int n, int kg) {
+  return (uint32_t)((n >> 3) * 1024 + kg * 128 + (n & 7) * 16);
+}
+}  // namespace
+
+template <int NP>
+__global__ void __launch_bounds__(kTcThreads, 1) summary_tc_kernel(ScanArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int C = (int)a.C, CC = C * C;
+  const int64_t N = a.N, E = N - 1, P = a.P, Ppad = a.Ppad, L = a.L;
+  const int64_t b = blockIdx.x / Ppad, k = blockIdx.x - (blockIdx.x / Ppad) * Ppad;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t node = b * a.nodes + k;
+  const int64_t len = seq_len(a.lengths, b, N);
+  const int64_t Eb = len < 0 ? 0 : len - 1;
+  const int64_t t0 = k * L;
+  const int64_t t1 = (t0 + L < Eb) ? t0 + L : Eb;
+  if ((k >= P) || (t0 >= Eb) || len < 0) {
+    if (tid == 0) {
+      a.ident[node] = 1;
+      a.cflag[b * Ppad + k] = 0;
+    }
+    return;
+  }
+  const int n = (int)(t1 - t0);
+  const float* potb = a.pot + b * E * (int64_t)CC;
+
+  float* wbuf = reinterpret_cast<float*>(smem + kOffW);
+  float* rsc = reinterpret_cast<float*>(smem + kOffRs);
+  float* Rp = reinterpret_cast<float*>(smem + kOffRp);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBar);
+  uint32_t* misc = reinterpret_cast<uint32_t*>(smem + kOffMisc);
+
+  if (warp == 8) tc::tmem_alloc<512>(&misc[0]);
+  if (tid == 0) {
+    for (int q = 0; q < 4; ++q) {
+      mbar_init(&bars[kBarFull + q], 32);
+      mbar_init(&bars[kBarEmpty + q], 1);
+      mbar_init(&bars[kBarStg + q], 1);
+    }
+    mbar_init(&bars[kBarW + 0], 128);
+    mbar_init(&bars[kBarW + 1], 128);
+    mbar_init(&bars[kBarD], 1);
+    mbar_init(&bars[kBarA], 128);
+    misc[1] = 0u;  // bit 0: non-finite input, bit 1: precision gate (cflag)
+    fence_mbar_init();
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tm = misc[0];
+  const uint32_t tD = tm, tAh = tm + 128, tAl = tm + 256;
+
+  if (warp >= 4 && warp < 8) {
+    // =============================== producers ===============================
+    const int pw = warp - 4, i0 = 32 * pw;
+    const int rows = (C - i0) < 0 ? 0 : ((C - i0) > 32 ? 32 : (C - i0));  // rows of this block
+    const float* stg = reinterpret_cast<const float*>(smem + kOffStg + pw * kBlk);
+    uint8_t* bhi = smem + kOffBhi + pw * kBlk;
+    uint8_t* blo = smem + kOffBlo + pw * kBlk;
+    const uint32_t blk_bytes = (uint32_t)(rows * C * 4);
+    bool bad = false, tiny = false;
+    if (lane == 0 && rows > 0)
+      bulk_load(smem + kOffStg + pw * kBlk, potb + t0 * CC + (int64_t)i0 * C, blk_bytes,
+                &bars[kBarStg + pw]);
+    for (int u = 0; u < n; ++u) {
+      // ---- tile u, rows i0.., columns j = 32 jb + lane; pass 1: row maxes ----------------
+      if (rows > 0) mbar_wait(&bars[kBarStg + pw], (uint32_t)(u & 1));
+      float rm[32];
+#pragma unroll
+      for (int rr = 0; rr < 32; ++rr) {
+        float m = neg_inf();
+#pragma unroll
+        for (int jb = 0; jb < 4; ++jb) {
+          const int j = 32 * jb + lane;
+          const float x = (rr < rows && j < C) ? stg[rr * C + j] : neg_inf();
+          bad |= (x != x) | (x == pos_inf());
+          m = fmaxf(m, x);
+        }
+        rm[rr] = m;
+      }
+      // 31-shuffle transpose reduction: lane L ends with the max of row i0 + L
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) {
+        const bool up = (lane & o) != 0;
+#pragma unroll
+        for (int q = 0; q < o; ++q) {
+          const float send = up ? rm[q] : rm[q + o];
+          const float keep = up ? rm[q + o] : rm[q];
+          rm[q] = fmaxf(keep, __shfl_xor_sync(0xffffffffu, send, o));
+        }
+      }
+      const float rmy = rm[0];
+      rsc[pw * 32 + lane] = rmy;
+      const float wmax = warp_max(rmy);
+      if (lane == 0) Rp[(u & 1) * 4 + pw] = wmax;
+      named_bar(1, 128);
+      float R = Rp[(u & 1) * 4 + 0];
+#pragma unroll
+      for (int q = 1; q < 4; ++q) R = fmaxf(R, Rp[(u & 1) * 4 + q]);
+      const float Rz = (R == neg_inf()) ? 0.f : R;
+      const float xw = (rmy - Rz) * kLog2e;
+      const float wv = (rmy == neg_inf()) ? 0.f : ex2(xw);
+      tiny |= (rmy != neg_inf()) & (xw < kTinyWtc);
+      // B stage p free (the MMA of tile u-1 is done with it)?
+      if (u > 0) mbar_wait(&bars[kBarEmpty + pw], (uint32_t)((u - 1) & 1));
+      wbuf[(u & 1) * 132 + i0 + lane] = wv;
+      if (pw == 0 && lane == 0) wbuf[(u & 1) * 132 + 128] = Rz;
+      mbar_arrive(&bars[kBarW + (u & 1)]);
+      // ---- pass 2: X = 2^((l - r_i) log2 e), split, K-major stores (4 k's per 16 B) ------
+#pragma unroll 2
+      for (int kg = 0; kg < 8; ++kg) {
+        float r[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) r[q] = rsc[pw * 32 + 4 * kg + q];
+#pragma unroll
+        for (int jb = 0; jb < 4; ++jb) {
+          const int j = 32 * jb + lane;
+          float e[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int rr = 4 * kg + q;
+            const float lv = (rr < rows && j < C) ? stg[rr * C + j] : neg_inf();
+            const float x = (lv - r[q]) * kLog2e;
+            tiny |= (x < kTinyXtc) & (x != neg_inf());
+            e[q] = (r[q] == neg_inf()) ? 0.f : ex2(x);
+          }
+          float4 h, l;
+          tc::split_tf32(e[0], h.x, l.x);
+          tc::split_tf32(e[1], h.y, l.y);
+          tc::split_tf32(e[2], h.z, l.z);
+          tc::split_tf32(e[3], h.w, l.w);
+          const uint32_t off = bstage_off(j, kg);
+          *reinterpret_cast<float4*>(bhi + off) = h;
+          if (NP == 3) *reinterpret_cast<float4*>(blo + off) = l;
+        }
+      }
+      // staging consumed: prefetch the next tile's block (generic reads before async write)
+      tc::fence_async_smem();
+      __syncwarp();
+      if (lane == 0 && rows > 0 && u + 1 < n)
+        bulk_load(smem + kOffStg + pw * kBlk, potb + (t0 + u + 1) * CC + (int64_t)i0 * C,
+                  blk_bytes, &bars[kBarStg + pw]);
+      tc::fence_async_smem();
+      mbar_arrive(&bars[kBarFull + pw]);
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&misc[1], 1u);
+    if (__any_sync(0xffffffffu, tiny) && lane == 0) atomicOr(&misc[1], 2u);
+  } else if (warp == 8) {
+    // =============================== MMA issuer ===============================
+    if (lane == 0) {
+      constexpr uint32_t idesc = tc::idesc_tf32(128, 128, 0, 0);
+      for (int u = 0; u < n; ++u) {
+        mbar_wait(&bars[kBarA], (uint32_t)(u & 1));
+        tc::fence_after();
+        for (int p = 0; p < 4; ++p) {
+          mbar_wait(&bars[kBarFull + p], (uint32_t)(u & 1));
+          tc::fence_after();
+          const uint8_t* bh = smem + kOffBhi + p * kBlk;
+          const uint8_t* bl = smem + kOffBlo + p * kBlk;
+#pragma unroll
+          for (int s = 0; s < 4; ++s) {
+            const uint32_t kc = (uint32_t)(32 * p + 8 * s);
+            const uint64_t dh = tc::smem_desc(bh + s * 256, 128, 1024);
+            tc::mma_tf32_ts(tD, tAh + kc, dh, idesc, (p | s) != 0);
+            if (NP == 3) {
+              const uint64_t dl = tc::smem_desc(bl + s * 256, 128, 1024);
+              tc::mma_tf32_ts(tD, tAh + kc, dl, idesc, 1u);
+              tc::mma_tf32_ts(tD, tAl + kc, dh, idesc, 1u);
+            }
+          }
+          tc::commit(&bars[kBarEmpty + p]);
+        }
+        tc::commit(&bars[kBarD]);
+      }
+    }
+    __syncwarp();
+  } else {
+    // =============================== epilogue ===============================
+    const int m = tid;  // row m <-> TMEM lane m
+    const uint32_t lb = (uint32_t)(32 * warp) << 16;
+    double off = 0.0;
+    bool dead = (m >= C);
+    bool tinyp = false;
+    // A_0 = diag(w^(0)) (the identity start, weighted by tile 0's row weights)
+    mbar_wait(&bars[kBarW + 0], 0u);
+    {
+      float wh, wl;
+      tc::split_tf32(dead ? 0.f : wbuf[m], wh, wl);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t vh[32], vl[32];
+#pragma unroll
+        for (int q = 0; q < 32; ++q) {
+          const bool d = (32 * c + q == m);
+          vh[q] = __float_as_uint(d ? wh : 0.f);
+          vl[q] = __float_as_uint(d ? wl : 0.f);
+        }
+        tc::st32(tAh + lb + 32 * c, vh);
+        if (NP == 3) tc::st32(tAl + lb + 32 * c, vl);
+      }
+      tc::wait_st();
+      tc::fence_before();
+      mbar_arrive(&bars[kBarA]);
+    }
+    float* S = a.mat + node * (int64_t)CC;
+    for (int u = 0; u < n; ++u) {
+      mbar_wait(&bars[kBarD], (uint32_t)(u & 1));
+      tc::fence_after();
+      float s = 0.f;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t v[32];
+        tc::ld32(tD + lb + 32 * c, v);
+#pragma unroll
+        for (int q = 0; q < 32; ++q) s += __uint_as_float(v[q]);
+      }
+      const float Ru = wbuf[(u & 1) * 132 + 128];
+      dead |= !(s > 0.f);
+      const float inv = dead ? 0.f : 1.f / s;
+      const float ls = dead ? 0.f : lg2(s);
+      if (!dead) off += (double)Ru + kLn2 * (double)ls;
+      if (u + 1 < n) {
+        const int nb = (u + 1) & 1;
+        mbar_wait(&bars[kBarW + nb], (uint32_t)(((u + 1) >> 1) & 1));
+        const float* w = wbuf + nb * 132;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t v[32], vh[32], vl[32];
+          tc::ld32(tD + lb + 32 * c, v);
+#pragma unroll
+          for (int q = 0; q < 32; ++q) {
+            const float p = __uint_as_float(v[q]) * inv;
+            tinyp |= (p > 0.f) & (p < kTinyPtc);
+            float h, l;
+            tc::split_tf32(p * w[32 * c + q], h, l);
+            vh[q] = __float_as_uint(h);
+            vl[q] = __float_as_uint(l);
+          }
+          tc::st32(tAh + lb + 32 * c, vh);
+          if (NP == 3) tc::st32(tAl + lb + 32 * c, vl);
+        }
+        tc::wait_st();
+        tc::fence_before();
+        mbar_arrive(&bars[kBarA]);
+      } else if (m < C) {
+        // final: leaf LogMat row m = log2 of the normalised row (+ fp64 natural offset)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t v[32];
+          tc::ld32(tD + lb + 32 * c, v);
+#pragma unroll
+          for (int q = 0; q < 32; ++q) {
+            const int j = 32 * c + q;
+            const float x = __uint_as_float(v[q]);
+            if (j < C) S[m * C + j] = (dead || !(x > 0.f)) ? neg_inf() : lg2(x) - ls;
+          }
+        }
+        a.off[node * (int64_t)C + m] = dead ? 0.0 : off;
+      }
+    }
+    if (__any_sync(0xffffffffu, tinyp) && lane == 0) atomicOr(&misc[1], 2u);
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  if (warp == 8) tc::tmem_dealloc<512>(tm);
+  if (tid == 0) {
+    const uint32_t f = misc[1];
+    a.ident[node] = 0;
+    a.cflag[b * Ppad + k] = (f & 2u) ? 1u : 0u;
+    if ((f & 1u) && a.wflags) atomicOr(&a.wflags[b], (unsigned)WF_NONFINITE);
+  }
+}
+
+namespace {
+std::atomic<int> g_tc_summary{3};  // 0 = SIMT summaries, 1 = 1xTF32, 3 = 3xTF32 (default)
+std::atomic<uint32_t> g_tc_attr{0};
+template <int NP>
+cudaError_t launch_np(const ScanArgs& a, cudaStream_t st) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint32_t bit = 1u << ((dev & 15) * 2 + (NP == 3 ? 1 : 0));
+  if (!(g_tc_attr.load() & bit)) {
+    cudaError_t e = cudaFuncSetAttribute(summary_tc_kernel<NP>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem);
+    if (e != cudaSuccess) return e;
+    g_tc_attr.fetch_or(bit);
+  }
+  summary_tc_kernel<NP><<<(unsigned)(a.B * a.Ppad), kTcThreads, kTcSmem, st>>>(a);
+  return cudaGetLastError();
+}
+}  // namespace
+
+bool summary_tc_ok(const ScanArgs& a) {
+  return g_tc_summary.load() != 0 && a.C > 64 && a.C <= 128 && (a.C % 2) == 0 &&
+         (reinterpret_cast<uintptr_t>(a.pot) & 15) == 0;
+}
+
+cudaError_t launch_summary_tc(const ScanArgs& a, cudaStream_t st) {
+  return g_tc_summary.load() == 1 ? launch_np<1>(a, st) : launch_np<3>(a, st);
+}
+
+void set_tc_summary(int mode) { g_tc_summary.store(mode == 1 || mode == 3 ? mode : 0); }
+int get_tc_summary() { return g_tc_summary.load(); }
+
+}  // namespace tsb

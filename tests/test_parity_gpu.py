@@ -212,17 +212,34 @@ def test_deterministic_bitwise(dev):
             assert torch.equal(x, y)
 
 
-def test_host_buffers_end_to_end(dev):
-    cfg = tsgen.CONFIGS[2]
-    pot = torch.from_numpy(tsgen.config_potentials(cfg)).pin_memory()
+@pytest.mark.parametrize("graphs", [True, False])
+@pytest.mark.parametrize("shape", [(32, 25, 20), (6, 200, 64), (3, 9, 5)])
+def test_host_buffers_end_to_end(dev, shape, graphs):
+    """ts_marginals_host: chunked pipeline, eager on the 1st sighting of a binding, captured
+    on the 2nd, graph replay after; fresh input contents in the same pinned buffers must be
+    read on every call (nothing cached but the launch sequence)."""
+    B, N, C = shape
+    pot = torch.empty((B, N - 1, C, C), dtype=torch.float32).pin_memory()
     marg = torch.empty_like(pot).pin_memory()
-    logz = torch.empty(cfg.B, dtype=torch.float32).pin_memory()
-    flags = torch.empty(cfg.B, dtype=torch.int32).pin_memory()
-    tsb.marginals_host(pot, marg, logz, flags, device=dev)
-    torch.cuda.synchronize()
-    lz_ref, mg_ref, _ = oracle.chain_marginals(pot.numpy())
-    check_logz(logz.numpy(), lz_ref)
-    check_marg(marg.numpy(), mg_ref)
+    logz = torch.empty(B, dtype=torch.float32).pin_memory()
+    flags = torch.empty(B, dtype=torch.int32).pin_memory()
+    lengths = torch.empty(B, dtype=torch.int32).pin_memory()
+    tsb.set_host_graphs(graphs)
+    try:
+        for call in range(4):
+            pot_np = tsgen.potentials(B, N, C, seed=100 + call)
+            len_np = tsgen.random_lengths(B, N, 7 + call)
+            pot.copy_(torch.from_numpy(pot_np))
+            lengths.copy_(torch.from_numpy(len_np))
+            tsb.marginals_host(pot, marg, logz, flags, lengths_host=lengths if call % 2 else None,
+                               device=dev)
+            torch.cuda.synchronize()
+            lz_ref, mg_ref, fl_ref = oracle.chain_marginals(pot_np, len_np if call % 2 else None)
+            check_logz(logz.numpy(), lz_ref)
+            check_marg(marg.numpy(), mg_ref)
+            np.testing.assert_array_equal(flags.numpy(), fl_ref)
+    finally:
+        tsb.set_host_graphs(True)
 
 
 @pytest.mark.parametrize("G", [2, 4])

@@ -99,3 +99,32 @@ def test_cfg5_shape_auto_plan_sampled(dev):
     lz_ref, mg_ref, _ = oracle.chain_marginals(pot, threads=4)
     check_logz(lz.cpu().numpy(), lz_ref)
     check_marg(marg.cpu().numpy(), mg_ref)
+
+
+@pytest.mark.parametrize("mode", [3, 1, 0])
+@pytest.mark.parametrize("B,N,C", [(2, 300, 128), (3, 200, 100), (2, 97, 66)])
+def test_tensor_core_summaries(dev, mode, B, N, C):
+    """Leaf summaries on tcgen05 (3 = 3xTF32, 1 = 1xTF32) vs the SIMT fp32 kernel (0): all
+    within the BASELINE gates of the fp64 oracle, chunked plans with ragged last chunks."""
+    tsb.set_tc_summary(mode)
+    try:
+        pot = tsgen.potentials(B, N, C, seed=70 + C + mode)
+        check_plan(pot, None, dev, [1, 7, 64])
+        pot = tsgen.tagging_potentials(B, N, C, seed=3, mask_frac=0.2)
+        lengths = tsgen.random_lengths(B, N, 11)
+        lengths[0] = N
+        check_plan(pot, lengths, dev, [5, 33])
+    finally:
+        tsb.set_tc_summary(3)
+
+
+@pytest.mark.parametrize("mode", [3, 1])
+def test_tensor_core_summaries_gate(dev, mode):
+    """Peaked tiles (entries ~ -90 nats) trip the precision gate; the exact kernel redoes them."""
+    tsb.set_tc_summary(mode)
+    try:
+        check_plan(tsgen.peaked_potentials(2, 60, 128, seed=9), None, dev, [4, 13])
+        check_plan(tsgen.large_offset_potentials(2, 60, 128, seed=2), None, dev, [6])
+        check_plan(20.0 * tsgen.potentials(2, 60, 128, seed=4), None, dev, [8])
+    finally:
+        tsb.set_tc_summary(3)

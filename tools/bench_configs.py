@@ -46,10 +46,12 @@ def main():
     ap.add_argument("--configs", default="2,3,4,5")
     ap.add_argument("--iters", type=int, default=5)
     ap.add_argument("--chunk", type=int, default=0)
+    ap.add_argument("--tc", type=int, default=3, help="leaf summaries: 3 3xTF32, 1 1xTF32, 0 SIMT")
     args = ap.parse_args()
     dev = torch.device("cuda:0")
     peak = peak_gbs()
     tsb.set_plan_chunk(args.chunk)
+    tsb.set_tc_summary(args.tc)
     for no in [int(x) for x in args.configs.split(",")]:
         cfg = tsgen.CONFIGS[no]
         B, N, C, E = cfg.B, cfg.N, cfg.C, cfg.E
@@ -68,7 +70,7 @@ def main():
         print(json.dumps({"config": f"cfg{no}", "op": cfg.op, "B": B, "N": N, "C": C,
                           "ms_median": med, "ms_best": best, "tokens_per_s": B * N / (med / 1e3),
                           "alg_bytes": alg, "achieved_gbs": gbs, "frac_hbm": gbs / peak,
-                          "launches": launches, "plan_chunk": args.chunk}), flush=True)
+                          "launches": launches, "plan_chunk": args.chunk, "tc": args.tc}), flush=True)
         del pot
         if cfg.op != "viterbi":
             del out
