@@ -26,6 +26,7 @@
 //   warp 8     TMEM allocation + the single MMA-issuing thread.
 // TMEM: D cols [0,128), A_hi [128,256), A_lo [256,384) (512 allocated; 1 CTA per SM).
 #include <atomic>
+#include <cstdio>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -55,6 +56,31 @@ constexpr float kTinyPtc = 9.313225746154785e-10f;  // 2^-30 normalised value
 // k-groups at LBO = 128 B, n-groups (8 columns) at SBO = 1024 B (32 k's per stage).
 __device__ __forceinline__ uint32_t bstage_off(int n, int kg) {
   return (uint32_t)((n >> 3) * 1024 + kg * 128 + (n & 7) * 16);
+}
+// mbarrier wait; with -DTS_TC_WATCHDOG a stuck wait reports (tag, u, block) and traps
+__device__ __forceinline__ void tc_wait(uint64_t* bar, uint32_t parity, int tag, int u) {
+#ifdef TS_TC_WATCHDOG
+  const uint32_t b = smem_u32(bar);
+  uint32_t done = 0;
+  const long long t_start = clock64();
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(b), "r"(parity)
+        : "memory");
+    if (!done && clock64() - t_start > 4000000000ll) {
+      printf("TC watchdog: block %d thread %d tag %d u %d parity %u\n", blockIdx.x, threadIdx.x,
+             tag, u, parity);
+      __trap();
+    }
+  } while (!done);
+#else
+  (void)tag;
+  (void)u;
+  mbar_wait(bar, parity);
+#endif
 }
 }  // namespace
 
@@ -120,7 +146,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) summary_tc_kernel(ScanArgs a) {
                 &bars[kBarStg + pw]);
     for (int u = 0; u < n; ++u) {
       // ---- tile u, rows i0.., columns j = 32 jb + lane; pass 1: row maxes ----------------
-      if (rows > 0) mbar_wait(&bars[kBarStg + pw], (uint32_t)(u & 1));
+      if (rows > 0) tc_wait(&bars[kBarStg + pw], (uint32_t)(u & 1), 1, u);
       float rm[32];
 #pragma unroll
       for (int rr = 0; rr < 32; ++rr) {
@@ -158,7 +184,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) summary_tc_kernel(ScanArgs a) {
       const float wv = (rmy == neg_inf()) ? 0.f : ex2(xw);
       tiny |= (rmy != neg_inf()) & (xw < kTinyWtc);
       // B stage p free (the MMA of tile u-1 is done with it)?
-      if (u > 0) mbar_wait(&bars[kBarEmpty + pw], (uint32_t)((u - 1) & 1));
+      if (u > 0) tc_wait(&bars[kBarEmpty + pw], (uint32_t)((u - 1) & 1), 2, u);
       wbuf[(u & 1) * 132 + i0 + lane] = wv;
       if (pw == 0 && lane == 0) wbuf[(u & 1) * 132 + 128] = Rz;
       mbar_arrive(&bars[kBarW + (u & 1)]);
@@ -206,10 +232,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) summary_tc_kernel(ScanArgs a) {
     if (lane == 0) {
       constexpr uint32_t idesc = tc::idesc_tf32(128, 128, 0, 0);
       for (int u = 0; u < n; ++u) {
-        mbar_wait(&bars[kBarA], (uint32_t)(u & 1));
+        tc_wait(&bars[kBarA], (uint32_t)(u & 1), 3, u);
         tc::fence_after();
         for (int p = 0; p < 4; ++p) {
-          mbar_wait(&bars[kBarFull + p], (uint32_t)(u & 1));
+          tc_wait(&bars[kBarFull + p], (uint32_t)(u & 1), 10 + p, u);
           tc::fence_after();
           const uint8_t* bh = smem + kOffBhi + p * kBlk;
           const uint8_t* bl = smem + kOffBlo + p * kBlk;
@@ -238,7 +264,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) summary_tc_kernel(ScanArgs a) {
     bool dead = (m >= C);
     bool tinyp = false;
     // A_0 = diag(w^(0)) (the identity start, weighted by tile 0's row weights)
-    mbar_wait(&bars[kBarW + 0], 0u);
+    tc_wait(&bars[kBarW + 0], 0u, 4, 0);
     {
       float wh, wl;
       tc::split_tf32(dead ? 0.f : wbuf[m], wh, wl);
@@ -260,7 +286,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) summary_tc_kernel(ScanArgs a) {
     }
     float* S = a.mat + node * (int64_t)CC;
     for (int u = 0; u < n; ++u) {
-      mbar_wait(&bars[kBarD], (uint32_t)(u & 1));
+      tc_wait(&bars[kBarD], (uint32_t)(u & 1), 5, u);
       tc::fence_after();
       float s = 0.f;
 #pragma unroll
@@ -277,7 +303,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) summary_tc_kernel(ScanArgs a) {
       if (!dead) off += (double)Ru + kLn2 * (double)ls;
       if (u + 1 < n) {
         const int nb = (u + 1) & 1;
-        mbar_wait(&bars[kBarW + nb], (uint32_t)(((u + 1) >> 1) & 1));
+        tc_wait(&bars[kBarW + nb], (uint32_t)(((u + 1) >> 1) & 1), 6, u);
         const float* w = wbuf + nb * 132;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
@@ -298,8 +324,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) summary_tc_kernel(ScanArgs a) {
         tc::wait_st();
         tc::fence_before();
         mbar_arrive(&bars[kBarA]);
-      } else if (m < C) {
-        // final: leaf LogMat row m = log2 of the normalised row (+ fp64 natural offset)
+      } else {
+        // final: leaf LogMat row m = log2 of the normalised row (+ fp64 natural offset).
+        // tcgen05.ld is .sync.aligned: every lane of the warp loads, rows >= C only skip
+        // the stores.
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           uint32_t v[32];
@@ -308,10 +336,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) summary_tc_kernel(ScanArgs a) {
           for (int q = 0; q < 32; ++q) {
             const int j = 32 * c + q;
             const float x = __uint_as_float(v[q]);
-            if (j < C) S[m * C + j] = (dead || !(x > 0.f)) ? neg_inf() : lg2(x) - ls;
+            if (m < C && j < C) S[m * C + j] = (dead || !(x > 0.f)) ? neg_inf() : lg2(x) - ls;
           }
         }
-        a.off[node * (int64_t)C + m] = dead ? 0.0 : off;
+        if (m < C) a.off[node * (int64_t)C + m] = dead ? 0.0 : off;
       }
     }
     if (__any_sync(0xffffffffu, tinyp) && lane == 0) atomicOr(&misc[1], 2u);
