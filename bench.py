@@ -227,6 +227,7 @@ def main():
     for k in range(args.warmup):
         step(k, st_handle)
     launches_per_step = tsb.last_launch_count()
+    kernel = tsb.last_kernel()
     torch.cuda.synchronize(dev)
 
     graph = None
@@ -306,8 +307,9 @@ def main():
         value = world * args.steps * cfg.tokens / (ms_max / 1e3)
         peak, peak_src = load_peaks()
         alg_bytes = 8 * B * E * C * C  # read l + write mu, per launch
-        kernel = "fb_small_kernel" if tsb.workspace_bytes(pots[0]) == 0 else "bwd_sweep_kernel"
-        launch_s = (ms / 1e3) / (args.steps * launches_per_step) if kernel == "fb_small_kernel" \
+        # the step is one launch of a fused kernel for the short-chain plans (cfg2): its
+        # average launch duration is the timed region / launches
+        launch_s = (ms / 1e3) / (args.steps * launches_per_step) if launches_per_step == 1 \
             else None
         achieved = (alg_bytes / launch_s / 1e9) if launch_s else None
         line = {

@@ -101,7 +101,8 @@ TS_API ts_status ts_logpartition(const ts_chain *c, ts_semiring s, float *logz, 
 
 /* Marginals dA/dl for TS_LOG; for TS_MAX the one-hot indicator of the
  * canonical argmax structure, d(A^*)/d(l).  marg [B][N-1][C][C] fp32 out
- * (16-byte aligned); logz [B] out or NULL; flags [B] out or NULL. */
+ * (16-byte aligned; may be NULL only when N == 1, i.e. no edges); logz [B] out (required
+ * for TS_LOG, may be NULL for TS_MAX); flags [B] out or NULL. */
 TS_API ts_status ts_marginals(const ts_chain *c, ts_semiring s, float *marg, float *logz,
                               uint32_t *flags, void *ws, size_t ws_bytes, void *stream);
 
@@ -180,6 +181,12 @@ TS_API int64_t ts_get_plan_chunk(void);
  * distributed shared memory (G in {2, 4}; 0 = the default one-CTA-per-sequence kernel). */
 TS_API void ts_set_small_cluster(int G);
 
+/* Debug/testing knob (process-global): 1 (default) runs short log-semiring chains with
+ * C % 4 == 0 and C <= 28 through the latency-optimised single-CTA kernel (bulk-copied
+ * tiles, lagged-normaliser sweeps, float4 marginals); 0 = the general single-CTA kernel.
+ * Results agree within the parity tolerances. */
+TS_API void ts_set_tiny(int enable);
+
 /* Debug/testing knob (process-global): 1 (default) runs ts_marginals for C = 64 with one
  * serial chunk per sequence as the meet-in-the-middle kernel (forward and backward
  * recursions concurrently from both ends, marginals fused); 0 = separate forward and
@@ -194,6 +201,10 @@ TS_API void ts_set_viterbi_split(int G);
 
 /* Number of kernel launches the most recent successful call on this host thread
  * enqueued (bench accounting). */
+/* Name of the dominant (time-wise) kernel enqueued by this thread's last successful
+ * ts_logpartition / ts_marginals / ts_viterbi call ("" before any): for measurement and
+ * profiling (bench.py roofline line).  Static string, never freed. */
+TS_API const char *ts_last_kernel(void);
 TS_API int ts_last_launch_count(void);
 
 TS_API const char *ts_status_str(ts_status s);

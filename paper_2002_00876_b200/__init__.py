@@ -268,6 +268,11 @@ def set_small_cluster(G: int) -> None:
     _lib.load().ts_set_small_cluster(int(G))
 
 
+def set_tiny(enable: bool) -> None:
+    """Debug knob: latency-optimised short-chain kernel for C % 4 == 0, C <= 28 (default on)."""
+    _lib.load().ts_set_tiny(1 if enable else 0)
+
+
 def set_meet(enable: bool) -> None:
     """Debug knob: meet-in-the-middle fused marginals kernel for C = 64 (default on)."""
     _lib.load().ts_set_meet(1 if enable else 0)
@@ -280,6 +285,11 @@ def set_viterbi_split(G: int) -> None:
 
 def get_plan_chunk() -> int:
     return int(_lib.load().ts_get_plan_chunk())
+
+
+def last_kernel() -> str:
+    """Dominant kernel of this thread's last hot-path call (measurement / profiling)."""
+    return _lib.load().ts_last_kernel().decode()
 
 
 def last_launch_count() -> int:

@@ -21,9 +21,10 @@ STATUS = {0: "TS_OK", 1: "TS_E_INVALID", 2: "TS_E_UNSUPPORTED", 3: "TS_E_WORKSPA
 SYMBOLS = ("ts_workspace_bytes", "ts_logpartition", "ts_marginals", "ts_viterbi",
            "ts_marginals_host", "ts_segment_summary_bytes", "ts_segment_summary",
            "ts_segment_finish", "ts_set_plan_chunk", "ts_get_plan_chunk", "ts_set_small_cluster",
+           "ts_set_tiny",
            "ts_set_meet", "ts_set_viterbi_split", "ts_set_host_graphs",
            "ts_host_alloc", "ts_host_free", "ts_set_tc_summary", "ts_get_tc_summary",
-           "ts_last_launch_count", "ts_status_str", "ts_version")
+           "ts_last_launch_count", "ts_last_kernel", "ts_status_str", "ts_version")
 
 
 class ts_chain(ctypes.Structure):
@@ -70,6 +71,10 @@ def load():
     L.ts_get_plan_chunk.restype = I64
     L.ts_set_small_cluster.argtypes = [INT]
     L.ts_set_small_cluster.restype = None
+    L.ts_last_kernel.argtypes = []
+    L.ts_last_kernel.restype = ctypes.c_char_p
+    L.ts_set_tiny.argtypes = [INT]
+    L.ts_set_tiny.restype = None
     L.ts_set_meet.argtypes = [INT]
     L.ts_set_meet.restype = None
     L.ts_set_viterbi_split.argtypes = [INT]

@@ -17,8 +17,10 @@ namespace {
 std::atomic<int64_t> g_plan_chunk{0};
 std::atomic<int> g_small_cluster{0};
 std::atomic<int> g_meet{1};
+std::atomic<int> g_tiny{1};    // short chains: 1 = fb_tiny when eligible, 0 = fb_small only
 std::atomic<int> g_vsplit{0};  // Viterbi: -1 one CTA per sequence, 0 auto, G forced cluster size  // meet-in-the-middle marginals kernel for C = 64  // debug: run short C<=32 chains on G-CTA clusters
 thread_local int t_launches = 0;
+thread_local const char* t_kernel = "";  // dominant kernel of the last call (bench / profiling)
 
 constexpr size_t kAlign = 256;
 inline size_t align_up(size_t x) { return (x + kAlign - 1) & ~(kAlign - 1); }
@@ -228,9 +230,17 @@ ts_status run_log(const ts_chain* c, float* marg, float* logz, uint32_t* flags, 
   if (p.kind == PlanKind::Small) {
     SmallArgs a{c->pot, c->lengths, c->B, c->N, c->C, marg, logz, flags};
     const int G = g_small_cluster.load();
-    ts_status r = (G > 1 && cluster_fits(c->N, c->C, G))
-                      ? cuda_status(launch_cluster(a, G, st))
-                      : cuda_status(launch_small(a, st));
+    ts_status r;
+    if (G > 1 && cluster_fits(c->N, c->C, G)) {
+      r = cuda_status(launch_cluster(a, G, st));
+      t_kernel = "fb_cluster_kernel";
+    } else if (g_tiny.load() && tiny_fits(a)) {
+      r = cuda_status(launch_tiny(a, st));
+      t_kernel = "fb_tiny_kernel";
+    } else {
+      r = cuda_status(launch_small(a, st));
+      t_kernel = "fb_small_kernel";
+    }
     if (r == TS_OK) t_launches = 1;
     return r;
   }
@@ -244,6 +254,7 @@ ts_status run_log(const ts_chain* c, float* marg, float* logz, uint32_t* flags, 
                w.alpha_hat, w.beta_hat, w.mlag, w.tmax};
     if ((e = launch_meet(m, c->C, st)) != cudaSuccess) return cuda_status(e);
     t_launches = 1;
+    t_kernel = "meet64_kernel";
     return TS_OK;
   }
   e = cudaMemsetAsync(w.wflags, 0, sizeof(uint32_t) * (size_t)c->B, st);
@@ -276,6 +287,7 @@ ts_status run_log(const ts_chain* c, float* marg, float* logz, uint32_t* flags, 
     sa.wflags = w.wflags;
     sa.logz = logz;
     sa.flags = flags;
+    t_kernel = summary_tc_ok(sa) ? "summary_tc_kernel" : "summary_fast_kernel";
     if ((e = launch_scan_up(sa, st, &n)) != cudaSuccess) return cuda_status(e);
     if (!marg) {  // logZ from the root of the Fig. 4 tree
       if ((e = launch_scan_logz(sa, st)) != cudaSuccess) return cuda_status(e);
@@ -306,6 +318,9 @@ ts_status run_log(const ts_chain* c, float* marg, float* logz, uint32_t* flags, 
   a.logz = logz;
   a.flags = flags;
   a.final_in_fwd = marg ? 0 : 1;
+  if (p.P == 1)
+    t_kernel = stream2_ok(a) ? (marg ? "bwd2_kernel" : "fwd2_kernel")
+                             : (marg ? "bwd_sweep_kernel" : "fwd_sweep_kernel");
   e = launch_fwd(a, st);
   if (e != cudaSuccess) return cuda_status(e);
   ++n;
@@ -340,6 +355,7 @@ ts_status run_max(const ts_chain* c, int op, float* marg, float* logz, int32_t* 
   int n = 0;
   ts_status r = cuda_status(launch_viterbi(a, st, &n, g_vsplit.load()));
   if (r == TS_OK) t_launches = n;
+  t_kernel = (g_vsplit.load() >= 0 && vit2_ok(a)) ? "vit2_kernel" : "viterbi_fwd_kernel";
   return r;
 }
 
@@ -540,8 +556,9 @@ TS_API ts_status ts_logpartition(const ts_chain* c, ts_semiring s, float* logz, 
 
 TS_API ts_status ts_marginals(const ts_chain* c, ts_semiring s, float* marg, float* logz,
                               uint32_t* flags, void* ws, size_t ws_bytes, void* stream) {
-  if (!chain_ok(c) || !marg || !aligned(marg, 16) || (logz && !aligned(logz, 4)) ||
-      (flags && !aligned(flags, 4)))
+  // N == 1: there are no edges, the marginal tensor is empty and `marg` may be NULL
+  if (!chain_ok(c) || (c->N > 1 && !marg) || (marg && !aligned(marg, 16)) ||
+      (logz && !aligned(logz, 4)) || (flags && !aligned(flags, 4)))
     return TS_E_INVALID;
   if (s != TS_LOG && s != TS_MAX) return TS_E_INVALID;
   if (!device_ok()) return TS_E_UNSUPPORTED;
@@ -780,7 +797,9 @@ TS_API int64_t ts_get_plan_chunk(void) { return g_plan_chunk.load(); }
 TS_API void ts_set_small_cluster(int G) {
   g_small_cluster.store((G == 2 || G == 4) ? G : 0);
 }
+TS_API void ts_set_tiny(int enable) { g_tiny.store(enable ? 1 : 0); }
 TS_API int ts_last_launch_count(void) { return t_launches; }
+TS_API const char* ts_last_kernel(void) { return t_kernel; }
 
 TS_API const char* ts_status_str(ts_status s) {
   switch (s) {

@@ -1,0 +1,110 @@
+"""GPU parity of the latency-optimised short-chain kernel (fb_tiny.cu: C % 4 == 0, C <= 28)
+against the fp64 oracle, and against the general single-CTA kernel (fb_small.cu) it
+replaces on those shapes.  Gates as everywhere: logZ 1e-5 relative,
+marginals 1e-4 absolute, flags identical.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2002_00876_b200 as tsb
+import tsgen
+from _util import check_logz, check_marg
+
+pytestmark = pytest.mark.gpu
+
+TINY_C = [4, 8, 12, 16, 20, 24, 28]
+
+
+@pytest.fixture
+def tiny_off():
+    tsb.set_tiny(False)
+    yield
+    tsb.set_tiny(True)
+
+
+def parity(pot_np, lengths_np, dev):
+    lz_ref, mg_ref, fl_ref = oracle.chain_marginals(pot_np, lengths_np, threads=8)
+    pot = torch.from_numpy(np.ascontiguousarray(pot_np)).to(dev)
+    lengths = (torch.from_numpy(lengths_np.astype(np.int32)).to(dev)
+               if lengths_np is not None else None)
+    m, lz, fl = tsb.marginals(pot, lengths)
+    check_logz(lz.cpu().numpy(), lz_ref)
+    assert (fl.cpu().numpy().astype(np.uint32) == fl_ref).all(), (fl.cpu().numpy(), fl_ref)
+    err = check_marg(m.cpu().numpy(), mg_ref)
+    lz2, fl2 = tsb.logpartition(pot, lengths)
+    check_logz(lz2.cpu().numpy(), lz_ref)
+    assert (fl2.cpu().numpy().astype(np.uint32) == fl_ref).all()
+    return err, m
+
+
+@pytest.mark.parametrize("C", TINY_C)
+@pytest.mark.parametrize("N", [1, 2, 3, 17, 25, 40])
+def test_tiny_shapes(dev, C, N):
+    pot = tsgen.potentials(3, N, C, seed=700 + 31 * C + N)
+    err, _ = parity(pot, None, dev)
+    assert err < 1e-5
+
+
+@pytest.mark.parametrize("C", [4, 20, 28])
+def test_tiny_lengths_and_flags(dev, C):
+    B, N = 9, 30
+    pot = tsgen.potentials(B, N, C, seed=C + 1)
+    lengths = tsgen.random_lengths(B, N, C)
+    lengths[0], lengths[1] = 1, N
+    pot[2] = -np.inf                   # EMPTY
+    pot[3, 4, 1, 2] = np.nan           # NONFINITE
+    pot[4, 0, 0, 0] = np.inf           # NONFINITE
+    lengths[5] = 0                     # BADLEN
+    lengths[6] = N + 3                 # BADLEN
+    lengths[2] = lengths[3] = lengths[4] = N
+    parity(pot, lengths, dev)
+
+
+@pytest.mark.parametrize("C", [8, 20])
+def test_tiny_masked_offset_peaked_wide(dev, C):
+    parity(tsgen.tagging_potentials(4, 25, C, seed=C, mask_frac=0.3), None, dev)
+    parity(tsgen.large_offset_potentials(3, 25, C, seed=C), None, dev)
+    parity(tsgen.peaked_potentials(3, 25, C, seed=C), None, dev)
+    parity(tsgen.wide_potentials(2, 25, C, seed=C, scale=20.0), None, dev)
+    base = tsgen.potentials(3, 25, C, seed=31, s=6)
+    for c in (1e4, -1e4):
+        parity((base + np.float32(c)).astype(np.float32), None, dev)
+
+
+@pytest.mark.parametrize("C", [4, 20])
+def test_tiny_hidden_path_gates(dev, C):
+    """A label reachable only through a column of -200 nats followed by a row of +200:
+    the linear sweep underflows there (EX = 0), so the exact log-space step (sweep gate)
+    and the exact log-space edge (marginal gate) must recover the path's mass."""
+    B, N = 4, 25
+    pot = tsgen.potentials(B, N, C, seed=77, s=10)
+    for b in range(B):
+        t, j = 5 + 3 * b, (b + 1) % C
+        pot[b, t, :, j] = -200.0
+        pot[b, t + 1, j, :] = 200.0 + pot[b, t + 1, j, :]
+    pot[3, 2, :, :] = -300.0 + pot[3, 2, :, :]      # a whole tile far below its neighbours
+    parity(pot.astype(np.float32), None, dev)
+
+
+def test_tiny_matches_general_kernel(dev, tiny_off):
+    for C in TINY_C:
+        pot = torch.from_numpy(tsgen.potentials(5, 25, C, seed=C)).to(dev)
+        tsb.set_tiny(False)
+        m0, l0, f0 = tsb.marginals(pot)
+        tsb.set_tiny(True)
+        m1, l1, f1 = tsb.marginals(pot)
+        assert torch.equal(f0, f1)
+        assert float((l0.double() - l1.double()).abs().max()) <= 1e-5 * float(l0.abs().max())
+        assert float((m0 - m1).abs().max()) <= 2e-6
+
+
+def test_tiny_cfg2_sum_to_one_and_deterministic(dev):
+    cfg = tsgen.CONFIGS[2]
+    pot = torch.from_numpy(tsgen.config_potentials(cfg)).to(dev)
+    m, lz, fl = tsb.marginals(pot)
+    s = m.double().sum(dim=(2, 3))
+    assert float((s - 1).abs().max()) < 1e-5
+    m2, lz2, fl2 = tsb.marginals(pot)
+    assert torch.equal(m, m2) and torch.equal(lz, lz2)

@@ -20,7 +20,7 @@ full() {  # cfg script-args kernel-regex name skip
   ncu -i $O/${TAG}_full_$4.ncu-rep --page raw --csv > $O/${TAG}_full_$4_raw.csv 2>/dev/null
   ncu -i $O/${TAG}_full_$4.ncu-rep --page details --csv > $O/${TAG}_full_$4_details.csv 2>/dev/null
 }
-full 2 "python bench.py --config 2 --steps 20 --warmup 5 --mode eager --no-cpu-baseline --e2e-steps 3" fb_small cfg2_fb_small 10
+full 2 "python bench.py --config 2 --steps 20 --warmup 5 --mode eager --no-cpu-baseline --e2e-steps 3" fb_tiny cfg2_fb_tiny 10
 full 3 "python tools/bench_configs.py --configs 3 --iters 2" meet64 cfg3_meet64 1
 full 4 "python tools/bench_configs.py --configs 4 --iters 2" vit2 cfg4_vit2 1
 for k in summary_tc fwd2 bwd2 tree_up; do
