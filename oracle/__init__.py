@@ -9,6 +9,7 @@ oracle/brute.py for the independent brute-force enumerator that pins it.
 from __future__ import annotations
 
 import ctypes
+import math
 import os
 
 import numpy as np
@@ -174,3 +175,104 @@ def max_indicator(path: np.ndarray, C: int, lengths=None) -> np.ndarray:
             if path[b, t] >= 0 and path[b, t + 1] >= 0:
                 out[b, t, path[b, t], path[b, t + 1]] = 1.0
     return out
+
+
+# ---------------------------------------------------------------------------------------
+# SURVEY §8(f) "next" rows: distribution properties of §3 on the same chain.
+# ---------------------------------------------------------------------------------------
+
+def chain_entropy(pot, lengths=None, threads: int = 1):
+    """Entropy H_b = -Σ_z p(z) log p(z) (Table 2 'Entropy' P:206) written out via
+    log p(z) = Score(z) - A and linearity of expectation over the parts:
+        H = A - E_p[Score(z)] = A - Σ_t Σ_ij mu_t[i][j] l_t[i][j]
+    fp64; terms with mu = 0 contribute 0 (masked -inf parts).  Flags as chain_marginals;
+    H = NaN for EMPTY / NONFINITE / BADLEN sequences.  -> (H [B] f64, logz [B], flags)."""
+    pot64 = np.asarray(pot, dtype=np.float64)
+    logz, marg, flags = chain_marginals(pot, lengths, want_marg=True, threads=threads)
+    B = pot64.shape[0]
+    H = np.empty(B, dtype=np.float64)
+    for b in range(B):
+        if flags[b] != 0:
+            H[b] = math.nan
+            continue
+        m = marg[b]
+        nz = m != 0.0
+        H[b] = logz[b] - float(np.sum(m[nz] * pot64[b][nz]))
+    return H, logz, flags
+
+
+def chain_score(pot, z, lengths=None):
+    """Score(z) = Σ_{t < len-1} l[t, z_t, z_{t+1}], fp64 (exact for fp32
+    inputs up to rounding of the sum).  z [B, N] int; a label outside [0, C) on a used
+    position gives NaN."""
+    pot64 = np.asarray(pot, dtype=np.float64)
+    z = np.asarray(z)
+    B, E, C, _ = pot64.shape
+    out = np.empty(B, dtype=np.float64)
+    for b in range(B):
+        n = E + 1 if lengths is None else int(lengths[b])
+        if n < 1 or n > E + 1 or np.any((z[b, :n] < 0) | (z[b, :n] >= C)):
+            out[b] = math.nan
+            continue
+        out[b] = math.fsum(pot64[b, t, z[b, t], z[b, t + 1]] for t in range(n - 1))
+    return out
+
+
+def chain_log_prob(pot, z, lengths=None, threads: int = 1):
+    """log p(z) = Score(z) - A (P:119 'Density')."""
+    logz, _, flags = chain_marginals(pot, lengths, want_marg=False, threads=threads)
+    sc = chain_score(pot, z, lengths)
+    out = sc - logz
+    out[flags != 0] = math.nan
+    return out
+
+
+def forward_alpha(pot_seq, n: int) -> np.ndarray:
+    """alpha [n, C] fp64 of one sequence: alpha_0 = 0, alpha_{t+1}[j] = LSE_i(alpha_t[i] +
+    l_t[i][j]) with the per-cell max of §6(c)."""
+    pot = np.asarray(pot_seq, dtype=np.float64)
+    C = pot.shape[-1]
+    al = np.zeros((n, C), dtype=np.float64)
+    for t in range(n - 1):
+        x = al[t][:, None] + pot[t]                      # [i, j]
+        q = np.max(x, axis=0)
+        with np.errstate(invalid="ignore", divide="ignore"):
+            s = np.sum(np.exp(x - np.where(np.isfinite(q), q, 0.0)[None, :]), axis=0)
+            al[t + 1] = np.where(np.isfinite(q), q + np.log(s), -math.inf)
+    return al
+
+
+def _draw(logw: np.ndarray, u: float) -> int:
+    """Inverse-CDF draw from p_i ∝ exp(logw_i): the smallest i with cdf_i > u (fp64)."""
+    m = float(np.max(logw))
+    p = np.exp(logw - m)
+    c = np.cumsum(p)
+    k = int(np.searchsorted(c, u * c[-1], side="right"))
+    return min(k, len(logw) - 1)
+
+
+def ffbs_sample(pot, uniforms, lengths=None):
+    """Forward-filtering backward-sampling (Table 2 'Sample' P:202): one exact draw
+    z ~ p(z) per (k, b) from caller-supplied uniforms u [K, B, N] in [0, 1):
+        z_{n-1} ~ p(z_{n-1}) ∝ exp(alpha_{n-1}[j])                      (u[k, b, n-1])
+        z_t     ~ p(z_t | z_{t+1}) ∝ exp(alpha_t[i] + l_t[i][z_{t+1}])   (u[k, b, t])
+    -> z [K, B, N] int32 (-1 beyond len or for EMPTY / NONFINITE / BADLEN sequences)."""
+    pot64 = np.asarray(pot, dtype=np.float64)
+    u = np.asarray(uniforms, dtype=np.float64)
+    K = u.shape[0]
+    B, E, C, _ = pot64.shape
+    N = E + 1
+    _, _, flags = chain_marginals(pot, lengths, want_marg=False)
+    z = np.full((K, B, N), -1, dtype=np.int32)
+    for b in range(B):
+        if flags[b] != 0:
+            continue
+        n = N if lengths is None else int(lengths[b])
+        al = forward_alpha(pot64[b], n)
+        for k in range(K):
+            zz = _draw(al[n - 1], u[k, b, n - 1])
+            z[k, b, n - 1] = zz
+            for t in range(n - 2, -1, -1):
+                zz = _draw(al[t] + pot64[b, t, :, zz], u[k, b, t])
+                z[k, b, t] = zz
+    return z

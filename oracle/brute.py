@@ -91,3 +91,17 @@ def optimal_set(pot_seq, n: int) -> np.ndarray:
 def count(n: int, C: int) -> int:
     """Count semiring on zero potentials (Table 2 'Count'): |Z| = C^n."""
     return labelings(n, C).shape[0]
+
+
+def probabilities(pot_seq, n: int) -> tuple[np.ndarray, np.ndarray]:
+    """(Z, p(z)) for every labelling: p = exp(Score - A)."""
+    Z, sc = scores(pot_seq, n)
+    A = _lse(sc)
+    return Z, np.exp(sc - A)
+
+
+def entropy(pot_seq, n: int) -> float:
+    """H = -Σ_z p(z) log p(z) by enumeration, terms with p = 0 omitted."""
+    _, p = probabilities(pot_seq, n)
+    p = p[p > 0]
+    return -math.fsum((p * np.log(p)).tolist())

@@ -290,18 +290,30 @@ __global__ void __launch_bounds__(kScanThreads) tree_up_kernel(ScanArgs a, int l
     if (tid == 0) a.ident[nd] = 0;
     return;
   }
-  const int CC4 = (CC + 3) & ~3;
-  float* W = sm;          // [C][C] row-adjusted S1
-  float* S2 = W + CC4;    // [C][C]
-  float* R = S2 + CC4;    // [C][C]
-  double* ref = reinterpret_cast<double*>(R + CC4);  // [C]
+  // Linear-space product (§6(c) exp-shifted form): with W[r][i] = (ln2 S1[r][i] + O2[i] -
+  // ref_r) log2 e <= 0 (ref_r = row max) and S2[i][j] <= 0,
+  //   R[r][j] = log2 Σ_i 2^W[r][i] 2^S2[i][j]
+  // is a real 128 x 128 x C GEMM of values in [0, 1] (8 x 8 register tile per thread).  A cell
+  // whose sum falls below 2^-60 may have lost significant terms to flush-to-zero and is
+  // recomputed exactly with the per-cell max from the global operands (the gate of §4).
+  constexpr int CP = 128;
+  float* wT = sm;            // [CP][CP] wT[i][r] = 2^W[r][i]
+  float* e2 = wT + CP * CP;  // [CP][CP] e2[i][j] = 2^S2[i][j]
+  float* R = e2 + CP * CP;   // [C][C] log2 results
+  double* ref = reinterpret_cast<double*>(R + CP * CP);  // [C]
   const float* S1g = a.mat + n1 * CC;
   const double* O1 = a.off + n1 * C;
   const float* S2g = a.mat + n2 * CC;
   const double* O2 = a.off + n2 * C;
-  for (int q = tid; q < CC; q += kScanThreads) S2[q] = S2g[q];
-  // per row r: c_i = ln2*S1[r][i] + O2[i];  ref_r = max_i c_i;  W[r][i] = (c_i - ref_r) log2 e
-  for (int r = tid; r < C; r += kScanThreads) {
+  for (int q = tid; q < CP * CP; q += kScanThreads) {
+    const int i = q >> 7, j = q & (CP - 1);
+    e2[q] = (i < C && j < C) ? ex2(S2g[i * C + j]) : 0.f;
+  }
+  for (int r = tid; r < CP; r += kScanThreads) {
+    if (r >= C) {
+      for (int i = 0; i < CP; ++i) wT[i * CP + r] = 0.f;
+      continue;
+    }
     double m = -INFINITY;
     for (int i = 0; i < C; ++i) {
       const float s1 = S1g[r * C + i];
@@ -311,22 +323,70 @@ __global__ void __launch_bounds__(kScanThreads) tree_up_kernel(ScanArgs a, int l
       }
     }
     ref[r] = m;
-    for (int i = 0; i < C; ++i) {
-      const float s1 = S1g[r * C + i];
-      W[r * C + i] = (s1 == neg_inf() || m == -INFINITY)
-                         ? neg_inf()
-                         : (float)((kLn2 * (double)s1 + O2[i] - m) * (double)kLog2e);
+    for (int i = 0; i < CP; ++i) {
+      const float s1 = i < C ? S1g[r * C + i] : neg_inf();
+      wT[i * CP + r] = (s1 == neg_inf() || m == -INFINITY)
+                           ? 0.f
+                           : ex2((float)((kLn2 * (double)s1 + O2[i] - m) * (double)kLog2e));
     }
   }
   __syncthreads();
-  for (int q = tid; q < CC; q += kScanThreads) {
-    const int r = q / C, j = q - (q / C) * C;
-    float m = neg_inf();
-    for (int i = 0; i < C; ++i) m = fmaxf(m, W[r * C + i] + S2[i * C + j]);
-    float s = 0.f;
-    if (m != neg_inf())
-      for (int i = 0; i < C; ++i) s += ex2(W[r * C + i] + S2[i * C + j] - m);
-    R[q] = (m == neg_inf()) ? neg_inf() : m + lg2(s);
+  {
+    const int ty = tid >> 4, tx = tid & 15, r0 = 8 * ty, j0 = 8 * tx;
+    float acc[8][8];
+#pragma unroll
+    for (int x = 0; x < 8; ++x)
+#pragma unroll
+      for (int y = 0; y < 8; ++y) acc[x][y] = 0.f;
+    if (r0 < C && j0 < C) {
+      for (int i = 0; i < C; ++i) {
+        const float4 a0 = *reinterpret_cast<const float4*>(wT + i * CP + r0);
+        const float4 a1 = *reinterpret_cast<const float4*>(wT + i * CP + r0 + 4);
+        const float4 b0 = *reinterpret_cast<const float4*>(e2 + i * CP + j0);
+        const float4 b1 = *reinterpret_cast<const float4*>(e2 + i * CP + j0 + 4);
+        const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+        const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+        for (int x = 0; x < 8; ++x)
+#pragma unroll
+          for (int y = 0; y < 8; ++y) acc[x][y] = fmaf(av[x], bv[y], acc[x][y]);
+      }
+    }
+#pragma unroll
+    for (int x = 0; x < 8; ++x) {
+      const int r = r0 + x;
+#pragma unroll
+      for (int y = 0; y < 8; ++y) {
+        const int j = j0 + y;
+        if (r < C && j < C) {
+          float v;
+          if (acc[x][y] >= kGate) {
+            v = lg2(acc[x][y]);
+          } else {  // exact per-cell max (§6(c)) from the global operands
+            const double rr = ref[r];
+            float m = neg_inf();
+            for (int i = 0; i < C; ++i) {
+              const float s1 = S1g[r * C + i];
+              const float w = (s1 == neg_inf() || rr == -INFINITY)
+                                  ? neg_inf()
+                                  : (float)((kLn2 * (double)s1 + O2[i] - rr) * (double)kLog2e);
+              m = fmaxf(m, w + S2g[i * C + j]);
+            }
+            float sum = 0.f;
+            if (m != neg_inf())
+              for (int i = 0; i < C; ++i) {
+                const float s1 = S1g[r * C + i];
+                const float w = (s1 == neg_inf() || rr == -INFINITY)
+                                    ? neg_inf()
+                                    : (float)((kLn2 * (double)s1 + O2[i] - rr) * (double)kLog2e);
+                sum += ex2(w + S2g[i * C + j] - m);
+              }
+            v = (m == neg_inf()) ? neg_inf() : m + lg2(sum);
+          }
+          R[r * C + j] = v;
+        }
+      }
+    }
   }
   __syncthreads();
   for (int r = tid; r < C; r += kScanThreads) {
@@ -700,7 +760,10 @@ cudaError_t launch_fast(const ScanArgs& a, cudaStream_t st) {
 }
 }  // namespace
 
-size_t scan_mat_smem(int64_t C) { return (size_t)(3 * ((C * C + 3) & ~3)) * 4 + (size_t)C * 8 + 64; }
+size_t scan_mat_smem(int64_t C) {  // tree_up: 3 [128][128] fp32 buffers + fp64 row refs
+  (void)C;
+  return (size_t)(3 * 128 * 128) * 4 + (size_t)128 * 8 + 64;
+}
 
 cudaError_t launch_scan_up(const ScanArgs& a, cudaStream_t st, int* launches) {
   const int C = (int)a.C;

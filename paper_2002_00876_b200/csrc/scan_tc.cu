@@ -34,6 +34,18 @@
 
 namespace tsb {
 
+#ifdef TS_TC_TIMING
+__device__ long long g_tc_t[64][8];
+#define TCT(u, k)                                                      \
+  do {                                                                 \
+    if (blockIdx.x == 0 && (u) < 64) g_tc_t[(u)][(k)] = clock64();     \
+  } while (0)
+#else
+#define TCT(u, k) \
+  do {            \
+  } while (0)
+#endif
+
 namespace {
 constexpr int kTcThreads = 288;
 constexpr int kBlk = 16384;                 // one B stage (32 rows x 128 cols fp32), bytes
@@ -84,10 +96,12 @@ __device__ __forceinline__ void tc_wait(uint64_t* bar, uint32_t parity, int tag,
 }
 }  // namespace
 
-template <int NP>
+// CF = compile-time C (128: every producer block is 32 full rows, all index arithmetic folds
+// into immediates) or 0 for a runtime C in (64, 128).
+template <int NP, int CF>
 __global__ void __launch_bounds__(kTcThreads, 1) summary_tc_kernel(ScanArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  const int C = (int)a.C, CC = C * C;
+  const int C = CF ? CF : (int)a.C, CC = C * C;
   const int64_t N = a.N, E = N - 1, P = a.P, Ppad = a.Ppad, L = a.L;
   const int64_t b = blockIdx.x / Ppad, k = blockIdx.x - (blockIdx.x / Ppad) * Ppad;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -135,7 +149,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) summary_tc_kernel(ScanArgs a) {
   if (warp >= 4 && warp < 8) {
     // =============================== producers ===============================
     const int pw = warp - 4, i0 = 32 * pw;
-    const int rows = (C - i0) < 0 ? 0 : ((C - i0) > 32 ? 32 : (C - i0));  // rows of this block
+    const int rows = CF == 128 ? 32 : ((C - i0) < 0 ? 0 : ((C - i0) > 32 ? 32 : (C - i0)));
     const float* stg = reinterpret_cast<const float*>(smem + kOffStg + pw * kBlk);
     uint8_t* bhi = smem + kOffBhi + pw * kBlk;
     uint8_t* blo = smem + kOffBlo + pw * kBlk;
@@ -223,6 +237,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) summary_tc_kernel(ScanArgs a) {
         bulk_load(smem + kOffStg + pw * kBlk, potb + (t0 + u + 1) * CC + (int64_t)i0 * C,
                   blk_bytes, &bars[kBarStg + pw]);
       tc::fence_async_smem();
+      if (pw == 0 && lane == 0) TCT(u, 7);
       mbar_arrive(&bars[kBarFull + pw]);
     }
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&misc[1], 1u);
@@ -232,8 +247,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) summary_tc_kernel(ScanArgs a) {
     if (lane == 0) {
       constexpr uint32_t idesc = tc::idesc_tf32(128, 128, 0, 0);
       for (int u = 0; u < n; ++u) {
+        TCT(u, 0);
         tc_wait(&bars[kBarA], (uint32_t)(u & 1), 3, u);
         tc::fence_after();
+        TCT(u, 1);
         for (int p = 0; p < 4; ++p) {
           tc_wait(&bars[kBarFull + p], (uint32_t)(u & 1), 10 + p, u);
           tc::fence_after();
@@ -253,6 +270,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) summary_tc_kernel(ScanArgs a) {
           tc::commit(&bars[kBarEmpty + p]);
         }
         tc::commit(&bars[kBarD]);
+        TCT(u, 2);
       }
     }
     __syncwarp();
@@ -288,14 +306,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) summary_tc_kernel(ScanArgs a) {
     for (int u = 0; u < n; ++u) {
       tc_wait(&bars[kBarD], (uint32_t)(u & 1), 5, u);
       tc::fence_after();
-      float s = 0.f;
+      if (tid == 0) TCT(u, 3);
+      float s4[4] = {0.f, 0.f, 0.f, 0.f};  // 4 independent chains (not 128 dependent adds)
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         uint32_t v[32];
         tc::ld32(tD + lb + 32 * c, v);
 #pragma unroll
-        for (int q = 0; q < 32; ++q) s += __uint_as_float(v[q]);
+        for (int q = 0; q < 32; ++q) s4[q & 3] += __uint_as_float(v[q]);
       }
+      const float s = (s4[0] + s4[1]) + (s4[2] + s4[3]);
       const float Ru = wbuf[(u & 1) * 132 + 128];
       dead |= !(s > 0.f);
       const float inv = dead ? 0.f : 1.f / s;
@@ -303,7 +323,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) summary_tc_kernel(ScanArgs a) {
       if (!dead) off += (double)Ru + kLn2 * (double)ls;
       if (u + 1 < n) {
         const int nb = (u + 1) & 1;
+        if (tid == 0) TCT(u, 4);
         tc_wait(&bars[kBarW + nb], (uint32_t)(((u + 1) >> 1) & 1), 6, u);
+        if (tid == 0) TCT(u, 5);
         const float* w = wbuf + nb * 132;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
@@ -323,6 +345,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) summary_tc_kernel(ScanArgs a) {
         }
         tc::wait_st();
         tc::fence_before();
+        if (tid == 0) TCT(u, 6);
         mbar_arrive(&bars[kBarA]);
       } else {
         // final: leaf LogMat row m = log2 of the normalised row (+ fp64 natural offset).
@@ -358,19 +381,19 @@ __global__ void __launch_bounds__(kTcThreads, 1) summary_tc_kernel(ScanArgs a) {
 
 namespace {
 std::atomic<int> g_tc_summary{3};  // 0 = SIMT summaries, 1 = 1xTF32, 3 = 3xTF32 (default)
-std::atomic<uint32_t> g_tc_attr{0};
-template <int NP>
+std::atomic<uint64_t> g_tc_attr2{0};
+template <int NP, int CF>
 cudaError_t launch_np(const ScanArgs& a, cudaStream_t st) {
   int dev = 0;
   cudaGetDevice(&dev);
-  const uint32_t bit = 1u << ((dev & 15) * 2 + (NP == 3 ? 1 : 0));
-  if (!(g_tc_attr.load() & bit)) {
-    cudaError_t e = cudaFuncSetAttribute(summary_tc_kernel<NP>,
+  const uint64_t bit = 1ull << ((dev & 15) * 4 + (NP == 3 ? 1 : 0) + (CF ? 2 : 0));
+  if (!(g_tc_attr2.load() & bit)) {
+    cudaError_t e = cudaFuncSetAttribute(summary_tc_kernel<NP, CF>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem);
     if (e != cudaSuccess) return e;
-    g_tc_attr.fetch_or(bit);
+    g_tc_attr2.fetch_or(bit);
   }
-  summary_tc_kernel<NP><<<(unsigned)(a.B * a.Ppad), kTcThreads, kTcSmem, st>>>(a);
+  summary_tc_kernel<NP, CF><<<(unsigned)(a.B * a.Ppad), kTcThreads, kTcSmem, st>>>(a);
   return cudaGetLastError();
 }
 }  // namespace
@@ -381,7 +404,9 @@ bool summary_tc_ok(const ScanArgs& a) {
 }
 
 cudaError_t launch_summary_tc(const ScanArgs& a, cudaStream_t st) {
-  return g_tc_summary.load() == 1 ? launch_np<1>(a, st) : launch_np<3>(a, st);
+  if (a.C == 128)
+    return g_tc_summary.load() == 1 ? launch_np<1, 128>(a, st) : launch_np<3, 128>(a, st);
+  return g_tc_summary.load() == 1 ? launch_np<1, 0>(a, st) : launch_np<3, 0>(a, st);
 }
 
 void set_tc_summary(int mode) { g_tc_summary.store(mode == 1 || mode == 3 ? mode : 0); }

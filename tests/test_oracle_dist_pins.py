@@ -1,0 +1,137 @@
+"""Pins for the oracle's distribution properties (entropy,
+density / log_prob, forward-filtering backward-sampling; §3, Table 2
+P:202-206) against things other than the oracle itself: brute-force enumeration of
+every labelling (P:149 footnote), closed forms of the definitions, and exact sampling
+frequencies.  A plausible bug (sign of the expectation term, conditioning on the wrong
+neighbour, an off-by-one position, a transposed tile) fails at least one test here.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import tsgen
+from oracle import brute
+
+CASES = [(1, 5, 3), (3, 2, 2), (2, 3, 4), (2, 6, 3), (1, 4, 6), (1, 1, 5)]
+
+
+@pytest.mark.parametrize("B,N,C", CASES)
+def test_entropy_matches_enumeration(B, N, C):
+    pot = tsgen.potentials(B, N, C, seed=2000 + 7 * N + C, s=8)
+    H, logz, flags = oracle.chain_entropy(pot)
+    assert (flags == 0).all()
+    for b in range(B):
+        assert abs(H[b] - brute.entropy(pot[b], N)) <= 1e-10 * max(1.0, abs(H[b]))
+
+
+def test_entropy_masked_and_lengths():
+    B, N, C = 4, 6, 3
+    pot = tsgen.tagging_potentials(B, N, C, seed=5, mask_frac=0.3)
+    lengths = np.array([6, 3, 1, 5], dtype=np.int32)
+    H, _, flags = oracle.chain_entropy(pot, lengths)
+    for b in range(B):
+        n = int(lengths[b])
+        assert abs(H[b] - brute.entropy(pot[b], n)) <= 1e-10 * max(1.0, abs(H[b]))
+    assert H[2] == pytest.approx(math.log(C), abs=1e-12)  # len 1: uniform over C labels
+
+
+def test_entropy_closed_forms():
+    # l = 0: p uniform over C^n labelings -> H = n ln C
+    for (N, C) in [(25, 20), (200, 7)]:
+        H, _, _ = oracle.chain_entropy(np.zeros((1, N - 1, C, C), np.float32))
+        assert H[0] == pytest.approx(N * math.log(C), rel=1e-12)
+    # separable l[t,i,j] = phi_t[j]: z_0 uniform, z_{t+1} ~ softmax(phi_t) independently
+    rng = np.random.default_rng(3)
+    N, C = 50, 9
+    phi = rng.standard_normal((N - 1, C)).astype(np.float32)
+    pot = np.broadcast_to(phi[:, None, :], (N - 1, C, C)).astype(np.float32)[None]
+    H, _, _ = oracle.chain_entropy(pot)
+    ref = math.log(C)
+    for t in range(N - 1):
+        p = np.exp(phi[t].astype(np.float64) - phi[t].max())
+        p /= p.sum()
+        ref -= float(np.sum(p * np.log(p)))
+    assert H[0] == pytest.approx(ref, rel=1e-12)
+
+
+def test_entropy_flags():
+    pot = tsgen.potentials(3, 5, 3, seed=1)
+    pot[0] = -np.inf
+    pot[1, 2, 0, 0] = np.nan
+    H, _, flags = oracle.chain_entropy(pot)
+    assert math.isnan(H[0]) and math.isnan(H[1]) and not math.isnan(H[2])
+    assert flags[0] == oracle.F_EMPTY and flags[1] == oracle.F_NONFINITE
+
+
+@pytest.mark.parametrize("B,N,C", CASES)
+def test_log_prob_matches_enumeration_and_normalises(B, N, C):
+    pot = tsgen.potentials(B, N, C, seed=3000 + N + C, s=8)
+    for b in range(B):
+        Z, p = brute.probabilities(pot[b], N)
+        z = np.broadcast_to(np.zeros((1, N), np.int32), (B, N)).copy()
+        lp_all = []
+        for zz in Z:
+            z[b] = zz
+            lp_all.append(oracle.chain_log_prob(pot, z)[b])
+        lp_all = np.array(lp_all)
+        np.testing.assert_allclose(lp_all, np.log(p), rtol=0, atol=1e-10)
+        assert math.fsum(np.exp(lp_all).tolist()) == pytest.approx(1.0, abs=1e-12)
+
+
+def test_score_paper_two_edge_example_and_bad_labels():
+    # Score of z = (c1, c2, c3) is l_{1,c1,c2} + l_{2,c2,c3}
+    pot = tsgen.potentials(1, 3, 4, seed=9, s=8)
+    z = np.array([[3, 1, 2]], np.int32)
+    assert oracle.chain_score(pot, z)[0] == float(pot[0, 0, 3, 1]) + float(pot[0, 1, 1, 2])
+    z_bad = np.array([[3, 4, 2]], np.int32)
+    assert math.isnan(oracle.chain_score(pot, z_bad)[0])
+    # positions beyond len are ignored
+    z_tail = np.array([[3, 1, -7]], np.int32)
+    assert oracle.chain_score(pot, z_tail, np.array([2], np.int32))[0] == float(pot[0, 0, 3, 1])
+
+
+def test_forward_alpha_gives_logz():
+    pot = tsgen.potentials(2, 30, 5, seed=4)
+    logz, _, _ = oracle.chain_marginals(pot)
+    for b in range(2):
+        al = oracle.forward_alpha(pot[b], 30)
+        m = al[-1].max()
+        assert m + math.log(np.exp(al[-1] - m).sum()) == pytest.approx(logz[b], rel=1e-13)
+
+
+def test_ffbs_frequencies_match_enumeration():
+    """Exact sampling: empirical frequencies of 60k draws vs p(z) by enumeration (TV < 0.02,
+    SURVEY §8(f) f2) for a 3-position, 3-label chain (27 labelings)."""
+    N, C, K = 3, 3, 60000
+    pot = tsgen.potentials(1, N, C, seed=11, s=6)
+    rng = np.random.default_rng(12)
+    u = rng.random((K, 1, N))
+    z = oracle.ffbs_sample(pot, u)[:, 0, :]
+    Z, p = brute.probabilities(pot[0], N)
+    code = (z * np.array([1, C, C * C])).sum(axis=1)
+    freq = np.bincount(code, minlength=C ** N) / K
+    codes_enum = (Z * np.array([1, C, C * C])).sum(axis=1)
+    tv = 0.5 * np.abs(freq[codes_enum] - p).sum()
+    assert tv < 0.02, tv
+
+
+def test_ffbs_inverse_cdf_and_conditioning():
+    """Deterministic structure: u -> 0 picks the first label with nonzero probability,
+    u -> 1 the last; a chain whose edges force z_{t} = z_{t+1} (identity-like potentials)
+    yields constant paths; masked labels are never drawn."""
+    C, N = 4, 6
+    pot = np.full((1, N - 1, C, C), -np.inf, np.float32)
+    for t in range(N - 1):
+        np.fill_diagonal(pot[0, t], 0.0)  # only z_t = z_{t+1} allowed
+    u = np.random.default_rng(1).random((200, 1, N))
+    z = oracle.ffbs_sample(pot, u)[:, 0, :]
+    assert (z == z[:, :1]).all()
+    lo = oracle.ffbs_sample(pot, np.zeros((1, 1, N)))[0, 0]
+    hi = oracle.ffbs_sample(pot, np.full((1, 1, N), 1 - 1e-12))[0, 0]
+    assert (lo == 0).all() and (hi == C - 1).all()
+    # lengths: -1 beyond len; len 1 -> z_0 uniform over C
+    pot2 = tsgen.potentials(2, N, C, seed=3)
+    z2 = oracle.ffbs_sample(pot2, np.full((1, 2, N), 0.6), np.array([N, 1], np.int32))
+    assert (z2[0, 1, 1:] == -1).all() and z2[0, 1, 0] == 2  # floor(0.6 * 4)
