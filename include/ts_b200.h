@@ -76,7 +76,9 @@ enum {
   TS_OP_MARG = 1,      /* ts_marginals                                      */
   TS_OP_VITERBI = 2,   /* ts_viterbi                                        */
   TS_OP_MARG_HOST = 3, /* ts_marginals_host (adds device staging of I/O)    */
-  TS_OP_SEGMENT = 4    /* ts_segment_summary + ts_segment_finish            */
+  TS_OP_SEGMENT = 4,   /* ts_segment_summary + ts_segment_finish            */
+  TS_OP_ENTROPY = 5,   /* ts_entropy (TS_LOG)                               */
+  TS_OP_SAMPLE = 6     /* ts_sample (TS_LOG, C <= 128)                      */
 };
 
 /* One batch of chains.  N >= 1 positions (N-1 edges), 1 <= B, 1 <= C <= 256.
@@ -110,6 +112,36 @@ TS_API ts_status ts_marginals(const ts_chain *c, ts_semiring s, float *marg, flo
  * path [B][N] int32 out (-1 beyond len_b); score [B] fp32 out; flags [B] out or NULL. */
 TS_API ts_status ts_viterbi(const ts_chain *c, int32_t *path, float *score, uint32_t *flags,
                             void *ws, size_t ws_bytes, void *stream);
+
+/* ---- distribution properties (§3) ----------
+ *
+ * Entropy (Table 2 'Entropy') of p(z) = exp(Score(z) - A), written out through
+ * log p(z) = Score(z) - A and linearity of expectation over the parts
+ * (P:181-183):   H_b = A_b - Σ_{t,i,j} mu[b][t][i][j] l[b][t][i][j].
+ * Runs the ts_marginals(TS_LOG) hot path into `marg` (required, as ts_marginals) and `logz`
+ * (required), then a deterministic two-stage fp64 reduction of mu·l (terms with mu = 0
+ * skipped).  entropy [B] fp32 out; NaN for EMPTY / NONFINITE / BADLEN sequences.
+ * ws: ts_workspace_bytes(c, TS_OP_ENTROPY, TS_LOG) bytes, 256-byte aligned. */
+TS_API ts_status ts_entropy(const ts_chain *c, float *marg, float *logz, float *entropy,
+                            uint32_t *flags, void *ws, size_t ws_bytes, void *stream);
+
+/* Density: out[b] = Score_b(z) - logz[b] with Score(z) = Σ_{t < len-1}
+ * l[b][t][z_t][z_{t+1}] accumulated in fp64.  z [B][N] int32 labels
+ * (positions >= len ignored); logz [B] device (from ts_logpartition) or NULL, in which case
+ * out = Score(z).  out[b] = NaN when a used label is outside [0, C), len is bad, or logz[b]
+ * is not finite.  No workspace; asynchronous on `stream`. */
+TS_API ts_status ts_log_prob(const ts_chain *c, const int32_t *z, const float *logz,
+                             float *out, void *stream);
+
+/* Exact sampling by forward-filtering backward-sampling (Table 2 'Sample'):
+ * K independent draws z ~ p(z) per sequence.  The random numbers are INPUTS: uniforms
+ * [K][B][N] fp32 in [0, 1), u[k][b][t] drives the draw of z_t (inverse CDF: the smallest
+ * label whose inclusive prefix sum of p(z_t | z_{t+1}) exceeds u * total; z_{len-1} from
+ * p(z_{len-1})).  z [K][B][N] int32 out (-1 beyond len and for flagged sequences); logz [B]
+ * out (required); flags [B] out or NULL.  TS_LOG only, C <= 128 (TS_E_UNSUPPORTED above).
+ * ws: ts_workspace_bytes(c, TS_OP_SAMPLE, TS_LOG) bytes (forward node vectors [B][N][C]). */
+TS_API ts_status ts_sample(const ts_chain *c, const float *uniforms, int64_t K, int32_t *z,
+                           float *logz, uint32_t *flags, void *ws, size_t ws_bytes, void *stream);
 
 /* End-to-end variant of ts_marginals with HOST buffers: host_chain->pot / ->lengths and
  * host_marg / host_logz / host_flags are host pointers (pinned for overlap); the call

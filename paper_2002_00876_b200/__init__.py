@@ -134,6 +134,65 @@ def viterbi(pot: torch.Tensor, lengths=None, ws: Workspace | None = None):
     return path, score, flags
 
 
+def entropy(pot: torch.Tensor, lengths=None, ws: Workspace | None = None,
+            out: torch.Tensor | None = None):
+    """Entropy H = A - Σ mu·l of the CRF: (H [B], marg, logZ, flags)."""
+    L = _lib.load()
+    ch = _chain(pot, lengths)
+    B = pot.shape[0]
+    marg = out if out is not None else torch.empty_like(pot)
+    logz = torch.empty(B, dtype=torch.float32, device=pot.device)
+    H = torch.empty(B, dtype=torch.float32, device=pot.device)
+    flags = torch.empty(B, dtype=torch.int32, device=pot.device)
+    wp, wn = _ws(pot, ch, _lib.TS_OP_ENTROPY, _lib.TS_LOG, ws)
+    _lib.check(L.ts_entropy(ctypes.byref(ch), marg.data_ptr(), logz.data_ptr(), H.data_ptr(),
+                            flags.data_ptr(), wp, wn, _stream(pot.device)), "ts_entropy")
+    return H, marg, logz, flags
+
+
+def log_prob(pot: torch.Tensor, z: torch.Tensor, lengths=None, logz: torch.Tensor | None = None):
+    """log p(z) = Score(z) - A for labellings z [B, N] int32; with logz=None the
+    partition is computed first (ts_logpartition)."""
+    L = _lib.load()
+    ch = _chain(pot, lengths)
+    if logz is None:
+        logz, _ = logpartition(pot, lengths)
+    z = z.to(torch.int32).contiguous()
+    out = torch.empty(pot.shape[0], dtype=torch.float32, device=pot.device)
+    _lib.check(L.ts_log_prob(ctypes.byref(ch), z.data_ptr(), logz.data_ptr(), out.data_ptr(),
+                             _stream(pot.device)), "ts_log_prob")
+    return out
+
+
+def score(pot: torch.Tensor, z: torch.Tensor, lengths=None):
+    """Score(z) = Σ_t l[t, z_t, z_{t+1}] for labellings z [B, N]."""
+    L = _lib.load()
+    ch = _chain(pot, lengths)
+    z = z.to(torch.int32).contiguous()
+    out = torch.empty(pot.shape[0], dtype=torch.float32, device=pot.device)
+    _lib.check(L.ts_log_prob(ctypes.byref(ch), z.data_ptr(), None, out.data_ptr(),
+                             _stream(pot.device)), "ts_log_prob")
+    return out
+
+
+def sample(pot: torch.Tensor, uniforms: torch.Tensor, lengths=None, ws: Workspace | None = None):
+    """K exact samples per sequence by forward-filtering backward-sampling
+    driven by caller-supplied uniforms [K, B, N] in [0, 1): (z [K, B, N] int32, logZ, flags)."""
+    L = _lib.load()
+    ch = _chain(pot, lengths)
+    u = uniforms.to(torch.float32).contiguous()
+    K = u.shape[0]
+    B, E = pot.shape[0], pot.shape[1]
+    assert u.shape == (K, B, E + 1), u.shape
+    z = torch.empty((K, B, E + 1), dtype=torch.int32, device=pot.device)
+    logz = torch.empty(B, dtype=torch.float32, device=pot.device)
+    flags = torch.empty(B, dtype=torch.int32, device=pot.device)
+    wp, wn = _ws(pot, ch, _lib.TS_OP_SAMPLE, _lib.TS_LOG, ws)
+    _lib.check(L.ts_sample(ctypes.byref(ch), u.data_ptr(), K, z.data_ptr(), logz.data_ptr(),
+                           flags.data_ptr(), wp, wn, _stream(pot.device)), "ts_sample")
+    return z, logz, flags
+
+
 _HOST_NEED: dict = {}
 
 

@@ -512,6 +512,30 @@ HostPipe* host_pipe() {
   return pipes[dev];
 }
 
+
+// ---- distribution properties ------------------------------------------
+size_t entropy_ws(const ts_chain* c, void* ws, size_t* marg_part, double** partial) {
+  const size_t m = align_up(op_ws(c, TS_OP_MARG, TS_LOG, nullptr, nullptr, nullptr));
+  DistArgs d{};
+  d.B = c->B;
+  d.N = c->N;
+  const int S = entropy_slices(d);
+  if (marg_part) *marg_part = m;
+  if (partial) *partial = ws ? reinterpret_cast<double*>(static_cast<char*>(ws) + m) : nullptr;
+  return m + align_up(sizeof(double) * (size_t)(c->B * S));
+}
+
+Plan serial_plan(const ts_chain* c) {
+  const int64_t E = c->N - 1;
+  return Plan{PlanKind::Stream, E > 0 ? E : 1, 1, 1, 0};
+}
+
+size_t sample_ws(const ts_chain* c, void* ws, StreamWs* w, uint32_t** fl) {
+  const size_t m = align_up(stream_ws(c, serial_plan(c), true, ws, w, nullptr));
+  if (fl) *fl = ws ? reinterpret_cast<uint32_t*>(static_cast<char*>(ws) + m) : nullptr;
+  return m + align_up(sizeof(uint32_t) * (size_t)c->B);
+}
+
 }  // namespace
 
 extern "C" {
@@ -539,8 +563,122 @@ TS_API size_t ts_workspace_bytes(const ts_chain* c, int op, ts_semiring s) {
     if (c->C > 128) return 0;
     return stream_ws(c, seg_plan(c), true, nullptr, nullptr, nullptr, true);
   }
+  if (op == TS_OP_ENTROPY) return s == TS_LOG ? entropy_ws(c, nullptr, nullptr, nullptr) : 0;
+  if (op == TS_OP_SAMPLE) return (s == TS_LOG && c->C <= 128) ? sample_ws(c, nullptr, nullptr, nullptr) : 0;
   if (op < TS_OP_LOGZ || op > TS_OP_VITERBI) return 0;
   return op_ws(c, op, s, nullptr, nullptr, nullptr);
+}
+
+TS_API ts_status ts_entropy(const ts_chain* c, float* marg, float* logz, float* entropy,
+                            uint32_t* flags, void* ws, size_t ws_bytes, void* stream) {
+  if (!chain_ok(c) || (c->N > 1 && !marg) || (marg && !aligned(marg, 16)) || !logz ||
+      !aligned(logz, 4) || !entropy || !aligned(entropy, 4) || (flags && !aligned(flags, 4)))
+    return TS_E_INVALID;
+  if (!device_ok()) return TS_E_UNSUPPORTED;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  size_t mpart = 0;
+  double* partial = nullptr;
+  const size_t need = entropy_ws(c, ws, &mpart, &partial);
+  if (ws_bytes < need || !ws || !aligned(ws, kAlign)) return TS_E_WORKSPACE;
+  ts_status r = run_log(c, marg, logz, flags, ws, mpart, st);
+  if (r != TS_OK) return r;
+  const int n = t_launches;
+  const char* k = t_kernel;
+  DistArgs d{};
+  d.pot = c->pot;
+  d.lengths = c->lengths;
+  d.B = c->B;
+  d.N = c->N;
+  d.C = c->C;
+  d.marg = marg;
+  d.logz = logz;
+  d.flags = flags;
+  d.out = entropy;
+  d.partial = partial;
+  r = cuda_status(launch_entropy(d, st));
+  if (r == TS_OK) {
+    t_launches = n + 2;
+    t_kernel = k;
+  }
+  return r;
+}
+
+TS_API ts_status ts_log_prob(const ts_chain* c, const int32_t* z, const float* logz, float* out,
+                             void* stream) {
+  if (!chain_ok(c) || !z || !aligned(z, 4) || !out || !aligned(out, 4) ||
+      (logz && !aligned(logz, 4)))
+    return TS_E_INVALID;
+  if (!device_ok()) return TS_E_UNSUPPORTED;
+  DistArgs d{};
+  d.pot = c->pot;
+  d.lengths = c->lengths;
+  d.B = c->B;
+  d.N = c->N;
+  d.C = c->C;
+  d.logz = logz;
+  d.z = z;
+  d.out = out;
+  ts_status r = cuda_status(launch_score(d, static_cast<cudaStream_t>(stream)));
+  if (r == TS_OK) {
+    t_launches = 1;
+    t_kernel = "score_kernel";
+  }
+  return r;
+}
+
+TS_API ts_status ts_sample(const ts_chain* c, const float* uniforms, int64_t K, int32_t* z,
+                           float* logz, uint32_t* flags, void* ws, size_t ws_bytes, void* stream) {
+  if (!chain_ok(c) || !uniforms || !aligned(uniforms, 4) || K < 1 || K > ((int64_t)1 << 31) ||
+      !z || !aligned(z, 4) || !logz || !aligned(logz, 4) || (flags && !aligned(flags, 4)))
+    return TS_E_INVALID;
+  if (c->C > 128) return TS_E_UNSUPPORTED;
+  if (!device_ok()) return TS_E_UNSUPPORTED;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  StreamWs w;
+  uint32_t* wfl = nullptr;
+  const size_t need = sample_ws(c, ws, &w, &wfl);
+  if (ws_bytes < need || !ws || !aligned(ws, kAlign)) return TS_E_WORKSPACE;
+  uint32_t* fl = flags ? flags : wfl;
+  cudaError_t e = cudaMemsetAsync(w.wflags, 0, sizeof(uint32_t) * (size_t)c->B, st);
+  if (e != cudaSuccess) return cuda_status(e);
+  // forward filtering: the serial streaming forward sweep (one chunk per sequence) stores
+  // every node vector; it also writes logZ and the flags (logZ-only epilogue)
+  SweepArgs a{};
+  a.pot = c->pot;
+  a.lengths = c->lengths;
+  a.B = c->B;
+  a.N = c->N;
+  a.C = c->C;
+  a.L = c->N - 1 > 0 ? c->N - 1 : 1;
+  a.P = 1;
+  a.alpha_hat = w.alpha_hat;
+  a.alpha_end = w.alpha_end;
+  a.alpha_end_off = w.alpha_end_off;
+  a.mlag = w.mlag;
+  a.tmax = w.tmax;
+  a.wflags = w.wflags;
+  a.logz = logz;
+  a.flags = fl;
+  a.final_in_fwd = 1;
+  if ((e = launch_fwd(a, st)) != cudaSuccess) return cuda_status(e);
+  DistArgs d{};
+  d.pot = c->pot;
+  d.lengths = c->lengths;
+  d.B = c->B;
+  d.N = c->N;
+  d.C = c->C;
+  d.flags = fl;
+  d.zout = z;
+  d.uniforms = uniforms;
+  d.K = K;
+  d.ah = w.alpha_hat;
+  d.aend = w.alpha_end;
+  ts_status r = cuda_status(launch_sample(d, st));
+  if (r == TS_OK) {
+    t_launches = 2;
+    t_kernel = "sample_kernel";
+  }
+  return r;
 }
 
 TS_API ts_status ts_logpartition(const ts_chain* c, ts_semiring s, float* logz, uint32_t* flags,

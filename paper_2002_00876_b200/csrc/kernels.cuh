@@ -149,4 +149,27 @@ cudaError_t launch_viterbi(const VitArgs& a, cudaStream_t st, int* launches, int
 bool vit2_ok(const VitArgs& a);
 cudaError_t launch_vit2(const VitArgs& a, int g_force, cudaStream_t st);
 
+// ---- distribution properties (dist_ops.cu) ---------------------------
+struct DistArgs {
+  const float* pot;
+  const int32_t* lengths;
+  int64_t B, N, C;
+  const float* marg;       // entropy: marginals [B][N-1][C][C]
+  const float* logz;       // [B] (entropy: required; score: NULL -> Score(z))
+  const uint32_t* flags;   // [B] or NULL
+  float* out;              // [B] entropy / log_prob
+  double* partial;         // entropy partials [B][S]
+  int64_t Ls;              // entropy slice length (edges)
+  const int32_t* z;        // score: labels [B][N]
+  int32_t* zout;           // sample: [K][B][N]
+  const float* uniforms;   // sample: [K][B][N]
+  int64_t K;
+  const float* ah;         // sample: forward node vectors [B][N][C] (log2, per-node frame)
+  const float* aend;       // sample: node Eb vector [B][C]
+};
+int entropy_slices(const DistArgs& a);
+cudaError_t launch_entropy(DistArgs a, cudaStream_t st);
+cudaError_t launch_score(const DistArgs& a, cudaStream_t st);
+cudaError_t launch_sample(const DistArgs& a, cudaStream_t st);
+
 }  // namespace tsb
