@@ -78,7 +78,8 @@ enum {
   TS_OP_MARG_HOST = 3, /* ts_marginals_host (adds device staging of I/O)    */
   TS_OP_SEGMENT = 4,   /* ts_segment_summary + ts_segment_finish            */
   TS_OP_ENTROPY = 5,   /* ts_entropy (TS_LOG)                               */
-  TS_OP_SAMPLE = 6     /* ts_sample (TS_LOG, C <= 128)                      */
+  TS_OP_SAMPLE = 6,    /* ts_sample (TS_LOG, C <= 128)                      */
+  TS_OP_SEGMENT_VITERBI = 7 /* ts_segment_viterbi_maps + _finish (same ws)   */
 };
 
 /* One batch of chains.  N >= 1 positions (N-1 edges), 1 <= B, 1 <= C <= 256.
@@ -112,6 +113,39 @@ TS_API ts_status ts_marginals(const ts_chain *c, ts_semiring s, float *marg, flo
  * path [B][N] int32 out (-1 beyond len_b); score [B] fp32 out; flags [B] out or NULL. */
 TS_API ts_status ts_viterbi(const ts_chain *c, int32_t *path, float *score, uint32_t *flags,
                             void *ws, size_t ws_bytes, void *stream);
+
+/* ---- time-sharded Viterbi (the max-plus form of the §6(a) scan,
+ * P:307-311, across devices; Table 2 'Max' P:200; tie rule R5) -------------------
+ * Each rank holds edges [edge_begin, edge_begin + local->N - 1) of every length-n_global
+ * chain (local->lengths must be NULL; C <= 128).  The caller performs two all-gathers on
+ * its NCCL group:
+ *   1. ts_segment_viterbi_summary: summary [B][C][C] fp32 (ts_segment_viterbi_summary_bytes)
+ *      = the max-plus product of the local edges, S[b][m][j] = best local path score from
+ *      label m at the first local node to label j at the last.
+ *      all_gather(summary -> all_summaries [world][B][C][C]).
+ *   2. ts_segment_viterbi_maps: combines all_summaries in a fixed order (identical on every
+ *      rank): boundary vector 0 (x) S_0 ... S_{rank-1}, global A* (score [B], optional) and
+ *      flags [B] (optional); runs the local forward with backpointers (kept in ws) and
+ *      writes maps [B][C] int32: the first-local-node label reached by backtracking from
+ *      each last-local-node label.   all_gather(maps -> all_maps [world][B][C]).
+ *   3. ts_segment_viterbi_finish (same ws): this rank's end label = maps_{rank+1}[...
+ *      maps_{world-1}[z_E]] (z_E = the smallest global argmax), then the local backtrack:
+ *      path [B][local->N] int32 (global nodes edge_begin .. edge_begin + local->N - 1;
+ *      -1 for EMPTY / NONFINITE sequences).
+ * With inputs whose partial path sums are exact in fp32 (the dyadic generator), the result
+ * equals the unsharded ts_viterbi bit for bit.  ws: ts_workspace_bytes(local,
+ * TS_OP_SEGMENT_VITERBI, TS_MAX) bytes, 256-byte aligned, shared by steps 2 and 3. */
+TS_API size_t ts_segment_viterbi_summary_bytes(const ts_chain *local);
+TS_API ts_status ts_segment_viterbi_summary(const ts_chain *local, int64_t edge_begin,
+                                            int64_t n_global, float *summary, void *stream);
+TS_API ts_status ts_segment_viterbi_maps(const ts_chain *local, int64_t edge_begin,
+                                         int64_t n_global, int rank, int world,
+                                         const float *all_summaries, int32_t *maps, float *score,
+                                         uint32_t *flags, void *ws, size_t ws_bytes, void *stream);
+TS_API ts_status ts_segment_viterbi_finish(const ts_chain *local, int64_t edge_begin,
+                                           int64_t n_global, int rank, int world,
+                                           const int32_t *all_maps, int32_t *path, void *ws,
+                                           size_t ws_bytes, void *stream);
 
 /* ---- distribution properties (§3) ----------
  *

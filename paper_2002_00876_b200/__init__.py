@@ -317,6 +317,67 @@ class Segment:
         return marg, logz, flags
 
 
+class ViterbiSegment:
+    """One rank's contiguous time segment for time-sharded Viterbi: the
+    max-plus summary, then (after gathering every rank's summary) the end-label maps, then
+    (after gathering the maps) the local path.  Holds the backpointer workspace between
+    maps() and finish()."""
+
+    def __init__(self, local_pot: torch.Tensor, edge_begin: int, n_global: int):
+        self.pot = local_pot
+        self.edge_begin = int(edge_begin)
+        self.n_global = int(n_global)
+        self.ch = _chain(local_pot, None)
+        L = _lib.load()
+        self.nbytes = int(L.ts_segment_viterbi_summary_bytes(ctypes.byref(self.ch)))
+        self.ws_bytes = int(L.ts_workspace_bytes(ctypes.byref(self.ch),
+                                                 _lib.TS_OP_SEGMENT_VITERBI, _lib.TS_MAX))
+        self.ws = Workspace(local_pot.device)
+        self.wptr = self.ws.ptr(self.ws_bytes)
+
+    def summary(self) -> torch.Tensor:
+        """Max-plus transfer matrices of the local edges [B, C, C] (Table 2 'Max')."""
+        L = _lib.load()
+        B, _, C, _ = self.pot.shape
+        out = torch.empty((B, C, C), dtype=torch.float32, device=self.pot.device)
+        _lib.check(L.ts_segment_viterbi_summary(ctypes.byref(self.ch), self.edge_begin,
+                                                self.n_global, out.data_ptr(),
+                                                _stream(self.pot.device)),
+                   "ts_segment_viterbi_summary")
+        return out
+
+    def maps(self, all_summaries: torch.Tensor, rank: int, world: int):
+        """-> (maps [B, C] int32, global score [B], flags [B])."""
+        L = _lib.load()
+        B, _, C, _ = self.pot.shape
+        dev = self.pot.device
+        all_summaries = all_summaries.contiguous()
+        maps = torch.empty((B, C), dtype=torch.int32, device=dev)
+        score = torch.empty(B, dtype=torch.float32, device=dev)
+        flags = torch.empty(B, dtype=torch.int32, device=dev)
+        _lib.check(L.ts_segment_viterbi_maps(ctypes.byref(self.ch), self.edge_begin,
+                                             self.n_global, int(rank), int(world),
+                                             all_summaries.data_ptr(), maps.data_ptr(),
+                                             score.data_ptr(), flags.data_ptr(), self.wptr,
+                                             self.ws_bytes, _stream(dev)),
+                   "ts_segment_viterbi_maps")
+        return maps, score, flags
+
+    def finish(self, all_maps: torch.Tensor, rank: int, world: int) -> torch.Tensor:
+        """-> local path [B, E_local + 1] int32 (global nodes edge_begin ...)."""
+        L = _lib.load()
+        B, E = self.pot.shape[0], self.pot.shape[1]
+        dev = self.pot.device
+        all_maps = all_maps.to(torch.int32).contiguous()
+        path = torch.empty((B, E + 1), dtype=torch.int32, device=dev)
+        _lib.check(L.ts_segment_viterbi_finish(ctypes.byref(self.ch), self.edge_begin,
+                                               self.n_global, int(rank), int(world),
+                                               all_maps.data_ptr(), path.data_ptr(), self.wptr,
+                                               self.ws_bytes, _stream(dev)),
+                   "ts_segment_viterbi_finish")
+        return path
+
+
 def set_plan_chunk(L: int) -> None:
     """Debug knob: 0 auto, 1 = pure Fig. 4 tree, >= N-1 = serial sweep."""
     _lib.load().ts_set_plan_chunk(int(L))

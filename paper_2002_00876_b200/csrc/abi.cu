@@ -536,6 +536,36 @@ size_t sample_ws(const ts_chain* c, void* ws, StreamWs* w, uint32_t** fl) {
   return m + align_up(sizeof(uint32_t) * (size_t)c->B);
 }
 
+
+// ---- time-sharded Viterbi segments (vseg.cu) ----------------------------------------------
+struct VsegWs {
+  uint8_t* bp = nullptr;
+  float* delta_in = nullptr;
+  float* lscore = nullptr;   // local forward's score (unused)
+  int32_t* lzend = nullptr;  // local forward's argmax, then this segment's end label
+  int32_t* zglob = nullptr;
+  float* gscore = nullptr;
+  uint32_t* gflags = nullptr;
+};
+size_t vseg_ws(const ts_chain* c, void* ws, VsegWs* out) {
+  Carve cv(ws);
+  VsegWs w;
+  const int64_t B = c->B, C = c->C, E = c->N - 1;
+  w.bp = cv.take<uint8_t>((size_t)(B * (E > 0 ? E : 1) * C));
+  w.delta_in = cv.take<float>((size_t)(B * C));
+  w.lscore = cv.take<float>((size_t)B);
+  w.lzend = cv.take<int32_t>((size_t)B);
+  w.zglob = cv.take<int32_t>((size_t)B);
+  w.gscore = cv.take<float>((size_t)B);
+  w.gflags = cv.take<uint32_t>((size_t)B);
+  if (out) *out = w;
+  return cv.off;
+}
+bool vseg_ok(const ts_chain* c, int64_t edge_begin, int64_t n_global) {
+  return chain_ok(c) && c->lengths == nullptr && edge_begin >= 0 &&
+         edge_begin + (c->N - 1) <= n_global - 1 && c->C <= 128;
+}
+
 }  // namespace
 
 extern "C" {
@@ -563,10 +593,123 @@ TS_API size_t ts_workspace_bytes(const ts_chain* c, int op, ts_semiring s) {
     if (c->C > 128) return 0;
     return stream_ws(c, seg_plan(c), true, nullptr, nullptr, nullptr, true);
   }
+  if (op == TS_OP_SEGMENT_VITERBI) return c->C <= 128 ? vseg_ws(c, nullptr, nullptr) : 0;
   if (op == TS_OP_ENTROPY) return s == TS_LOG ? entropy_ws(c, nullptr, nullptr, nullptr) : 0;
   if (op == TS_OP_SAMPLE) return (s == TS_LOG && c->C <= 128) ? sample_ws(c, nullptr, nullptr, nullptr) : 0;
   if (op < TS_OP_LOGZ || op > TS_OP_VITERBI) return 0;
   return op_ws(c, op, s, nullptr, nullptr, nullptr);
+}
+
+TS_API size_t ts_segment_viterbi_summary_bytes(const ts_chain* local) {
+  if (!chain_ok(local)) return 0;
+  return sizeof(float) * (size_t)(local->B * local->C * local->C);
+}
+
+TS_API ts_status ts_segment_viterbi_summary(const ts_chain* local, int64_t edge_begin,
+                                            int64_t n_global, float* summary, void* stream) {
+  if (!vseg_ok(local, edge_begin, n_global) || !summary || !aligned(summary, 16))
+    return TS_E_INVALID;
+  if (!device_ok()) return TS_E_UNSUPPORTED;
+  VsegArgs v{};
+  v.pot = local->pot;
+  v.B = local->B;
+  v.N = local->N;
+  v.C = local->C;
+  v.summary = summary;
+  ts_status r = cuda_status(launch_vseg_summary(v, static_cast<cudaStream_t>(stream)));
+  if (r == TS_OK) {
+    t_launches = 1;
+    t_kernel = "vseg_summary_kernel";
+  }
+  return r;
+}
+
+TS_API ts_status ts_segment_viterbi_maps(const ts_chain* local, int64_t edge_begin,
+                                         int64_t n_global, int rank, int world,
+                                         const float* all_summaries, int32_t* maps, float* score,
+                                         uint32_t* flags, void* ws, size_t ws_bytes, void* stream) {
+  if (!vseg_ok(local, edge_begin, n_global) || world < 1 || rank < 0 || rank >= world ||
+      !all_summaries || !maps || !aligned(maps, 4) || (score && !aligned(score, 4)) ||
+      (flags && !aligned(flags, 4)))
+    return TS_E_INVALID;
+  if (!device_ok()) return TS_E_UNSUPPORTED;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  VsegWs w;
+  const size_t need = vseg_ws(local, ws, &w);
+  if (ws_bytes < need || !ws || !aligned(ws, kAlign)) return TS_E_WORKSPACE;
+  VsegArgs v{};
+  v.pot = local->pot;
+  v.B = local->B;
+  v.N = local->N;
+  v.C = local->C;
+  v.all_summ = all_summaries;
+  v.rank = rank;
+  v.world = world;
+  v.delta_in = w.delta_in;
+  v.score = w.gscore;
+  v.zglob = w.zglob;
+  v.flags = w.gflags;
+  v.bp = w.bp;
+  v.maps = maps;
+  cudaError_t e;
+  if ((e = launch_vseg_combine(v, st)) != cudaSuccess) return cuda_status(e);
+  VitArgs a{};
+  a.pot = local->pot;
+  a.B = local->B;
+  a.N = local->N;
+  a.C = local->C;
+  a.bp = w.bp;
+  a.zend = w.lzend;
+  a.score = w.lscore;
+  a.delta_in = w.delta_in;
+  if ((e = launch_vit1(a, st)) != cudaSuccess) return cuda_status(e);
+  if ((e = launch_vseg_maps(v, st)) != cudaSuccess) return cuda_status(e);
+  if (score && (e = cudaMemcpyAsync(score, w.gscore, sizeof(float) * (size_t)local->B,
+                                    cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
+    return cuda_status(e);
+  if (flags && (e = cudaMemcpyAsync(flags, w.gflags, sizeof(uint32_t) * (size_t)local->B,
+                                    cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
+    return cuda_status(e);
+  t_launches = 3;
+  t_kernel = "viterbi_fwd_kernel";
+  return TS_OK;
+}
+
+TS_API ts_status ts_segment_viterbi_finish(const ts_chain* local, int64_t edge_begin,
+                                           int64_t n_global, int rank, int world,
+                                           const int32_t* all_maps, int32_t* path, void* ws,
+                                           size_t ws_bytes, void* stream) {
+  if (!vseg_ok(local, edge_begin, n_global) || world < 1 || rank < 0 || rank >= world ||
+      !all_maps || !path || !aligned(path, 4))
+    return TS_E_INVALID;
+  if (!device_ok()) return TS_E_UNSUPPORTED;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  VsegWs w;
+  const size_t need = vseg_ws(local, ws, &w);
+  if (ws_bytes < need || !ws || !aligned(ws, kAlign)) return TS_E_WORKSPACE;
+  VsegArgs v{};
+  v.B = local->B;
+  v.N = local->N;
+  v.C = local->C;
+  v.rank = rank;
+  v.world = world;
+  v.zglob = w.zglob;
+  v.all_maps = all_maps;
+  v.zend = w.lzend;
+  cudaError_t e;
+  if ((e = launch_vseg_endlabel(v, st)) != cudaSuccess) return cuda_status(e);
+  VitArgs a{};
+  a.pot = local->pot;
+  a.B = local->B;
+  a.N = local->N;
+  a.C = local->C;
+  a.bp = w.bp;
+  a.zend = w.lzend;
+  a.path = path;
+  if ((e = launch_backtrack(a, st)) != cudaSuccess) return cuda_status(e);
+  t_launches = 2;
+  t_kernel = "backtrack_kernel";
+  return TS_OK;
 }
 
 TS_API ts_status ts_entropy(const ts_chain* c, float* marg, float* logz, float* entropy,

@@ -140,11 +140,14 @@ struct VitArgs {
   int32_t* path;    // [B][N] or nullptr
   float* marg;      // [B][N-1][C][C] indicator or nullptr
   float* logz;      // [B] copy of the score for ts_logpartition/ts_marginals(TS_MAX), or nullptr
+  const float* delta_in;  // [B][C] start vector (time-sharded segment), or nullptr (= 0)
 };
 size_t vit_smem_bytes(int64_t C, int stages, int rows_per_stage);
 // vsplit: -1 = one-CTA-per-sequence kernel for every C; 0 = auto (cluster column split for
 // C in {128, 256}); 1/2/4/8 = forced cluster size for C in {128, 256}.
 cudaError_t launch_viterbi(const VitArgs& a, cudaStream_t st, int* launches, int vsplit);
+cudaError_t launch_backtrack(const VitArgs& a, cudaStream_t st);
+cudaError_t launch_vit1(const VitArgs& a, cudaStream_t st);
 // cluster column-split forward (viterbi2.cu)
 bool vit2_ok(const VitArgs& a);
 cudaError_t launch_vit2(const VitArgs& a, int g_force, cudaStream_t st);
@@ -171,5 +174,26 @@ int entropy_slices(const DistArgs& a);
 cudaError_t launch_entropy(DistArgs a, cudaStream_t st);
 cudaError_t launch_score(const DistArgs& a, cudaStream_t st);
 cudaError_t launch_sample(const DistArgs& a, cudaStream_t st);
+
+// ---- time-sharded Viterbi segments (vseg.cu) -------------------------------
+struct VsegArgs {
+  const float* pot;       // local edges [B][E_loc][C][C]
+  int64_t B, N, C;        // local chain (N = E_loc + 1 nodes)
+  float* summary;         // [B][C][C] max-plus transfer matrix of the local edges
+  const float* all_summ;  // [world][B][C][C]
+  int rank, world;
+  float* delta_in;        // [B][C] boundary vector of this segment
+  float* score;           // [B] global A*
+  int32_t* zglob;         // [B] global final label (first argmax)
+  uint32_t* flags;        // [B] or nullptr
+  const uint8_t* bp;      // local backpointers [B][E_loc][C]
+  int32_t* maps;          // [B][C] end label -> start label of the local segment
+  const int32_t* all_maps;  // [world][B][C]
+  int32_t* zend;          // [B] this segment's end label
+};
+cudaError_t launch_vseg_summary(const VsegArgs& a, cudaStream_t st);
+cudaError_t launch_vseg_combine(const VsegArgs& a, cudaStream_t st);
+cudaError_t launch_vseg_maps(const VsegArgs& a, cudaStream_t st);
+cudaError_t launch_vseg_endlabel(const VsegArgs& a, cudaStream_t st);
 
 }  // namespace tsb

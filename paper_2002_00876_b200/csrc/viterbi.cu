@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(256) viterbi_fwd_kernel(VitArgs a, int S, int 
   };
 
   for (int u = 0; u < S - 1; ++u) issue(u);
-  dl[tid] = act ? 0.f : neg_inf();
+  dl[tid] = act ? (a.delta_in ? a.delta_in[b * C + tid] : 0.f) : neg_inf();
   float best = neg_inf(), chk = neg_inf();
   int arg = 0;
   int buf = 0;
@@ -269,7 +269,7 @@ cudaError_t set_smem(K kern, int bit) {
 
 cudaError_t launch_viterbi(const VitArgs& a, cudaStream_t st, int* launches, int vsplit) {
   cudaError_t e;
-  if (vsplit >= 0 && vit2_ok(a)) {
+  if (vsplit >= 0 && vit2_ok(a) && !a.delta_in) {
     if ((e = launch_vit2(a, vsplit, st)) != cudaSuccess) return e;
   } else {
     if ((e = launch_vit1(a, st)) != cudaSuccess) return e;
@@ -288,6 +288,13 @@ cudaError_t launch_viterbi(const VitArgs& a, cudaStream_t st, int* launches, int
   }
   if (launches) *launches = n;
   return cudaSuccess;
+}
+
+cudaError_t launch_backtrack(const VitArgs& a, cudaStream_t st) {
+  cudaError_t e = set_smem(backtrack_kernel, 2);
+  if (e != cudaSuccess) return e;
+  backtrack_kernel<<<(unsigned)a.B, 32, kBtSmem, st>>>(a);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_vit1(const VitArgs& a, cudaStream_t st) {

@@ -78,6 +78,39 @@ def time_sharded_marginals(local_pot, edge_begin: int, n_global: int, group=None
     return ops.finish(gathered, rank, world, want_marg)
 
 
+class CudaViterbiSegmentOps:
+    """Default ops for time-sharded Viterbi: ts_segment_viterbi_summary / _maps / _finish."""
+
+    def __init__(self):
+        self.seg = None
+
+    def summary(self, local_pot, edge_begin, n_global):
+        from . import ViterbiSegment
+
+        self.seg = ViterbiSegment(local_pot, edge_begin, n_global)
+        return self.seg.summary()
+
+    def maps(self, gathered, rank, world):
+        return self.seg.maps(gathered, rank, world)
+
+    def finish(self, gathered_maps, rank, world):
+        return self.seg.finish(gathered_maps, rank, world)
+
+
+def time_sharded_viterbi(local_pot, edge_begin: int, n_global: int, group=None, ops=None):
+    """Viterbi of chains split in time across the ranks of `group`:
+    all-gather of the max-plus segment summaries, then of the [B, C] end-label maps.
+    Returns (local path [B, E_local + 1] covering global nodes edge_begin..., global score
+    [B], flags [B]); the score and flags are identical on every rank."""
+    ops = ops or CudaViterbiSegmentOps()
+    rank = dist.get_rank(group)
+    world = dist.get_world_size(group)
+    summ = ops.summary(local_pot, edge_begin, n_global)
+    maps, score, flags = ops.maps(_all_gather(summ, group), rank, world)
+    path = ops.finish(_all_gather(maps, group), rank, world)
+    return path, score, flags
+
+
 def batch_sharded(fn, pot_local, *args, **kw):
     """Batch sharding needs no collective: each rank runs `fn` on its own slice."""
     return fn(pot_local, *args, **kw)

@@ -113,3 +113,84 @@ def test_shard_ranges_partition():
                 assert b0 + c0 == b1
             assert sum(c for _, c in spans) == n
             assert max(c for _, c in spans) - min(c for _, c in spans) <= 1
+
+
+class OracleViterbiSegmentOps:
+    """fp64 reference of the Viterbi segment steps (max-plus summary, boundary vector, local
+    forward with first-index backpointers, end-label maps, local backtrack) — tests only."""
+
+    def summary(self, local_pot, edge_begin, n_global):
+        pot = local_pot.numpy()
+        self.pot = pot.astype(np.float64)
+        return torch.from_numpy(np.stack([oracle.chain_summary(pot[b], oracle.MAX)
+                                          for b in range(pot.shape[0])]))
+
+    def maps(self, gathered, rank, world):
+        S = gathered.numpy()
+        B, C = S.shape[1], S.shape[2]
+        self.bp, self.zE = [], []
+        maps = np.empty((B, C), np.int32)
+        score = np.empty(B)
+        for b in range(B):
+            v = np.zeros(C)
+            for g in range(world):
+                if g == rank:
+                    d = v.copy()
+                v = np.max(v[:, None] + S[g, b], axis=0)
+            score[b] = v.max()
+            self.zE.append(int(np.argmax(v)))           # first argmax (reading R5)
+            bps = []
+            for t in range(self.pot.shape[1]):
+                x = d[:, None] + self.pot[b, t]
+                bps.append(np.argmax(x, axis=0))        # smallest index on ties
+                d = np.max(x, axis=0)
+            self.bp.append(bps)
+            for j in range(C):
+                z = j
+                for t in range(len(bps) - 1, -1, -1):
+                    z = int(bps[t][z])
+                maps[b, j] = z
+        return torch.from_numpy(maps), torch.from_numpy(score), torch.zeros(B, dtype=torch.int32)
+
+    def finish(self, gathered_maps, rank, world):
+        M = gathered_maps.numpy()
+        B = M.shape[1]
+        E = self.pot.shape[1]
+        path = np.empty((B, E + 1), np.int32)
+        for b in range(B):
+            e = self.zE[b]
+            for g in range(world - 1, rank, -1):
+                e = int(M[g, b, e])
+            path[b, E] = e
+            for t in range(E - 1, -1, -1):
+                e = int(self.bp[b][t][e])
+                path[b, t] = e
+        return torch.from_numpy(path)
+
+
+def _vworker(rank, world, port, B, N, C, seed, result_dir):
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    try:
+        pot = (np.random.default_rng(seed).integers(-3, 4, size=(B, N - 1, C, C)) * 0.5
+               ).astype(np.float32)  # coarse: frequent exact ties
+        begin, count = tdist.shard_edges(N - 1, world, rank)
+        local = torch.from_numpy(np.ascontiguousarray(pot[:, begin:begin + count]))
+        path, score, flags = tdist.time_sharded_viterbi(local, begin, N,
+                                                        ops=OracleViterbiSegmentOps())
+        p_ref, s_ref, _ = oracle.chain_viterbi(pot)
+        ok_p = np.array_equal(path.numpy(), p_ref[:, begin:begin + count + 1])
+        ok_s = np.array_equal(score.numpy(), s_ref)
+        with open(os.path.join(result_dir, f"v{rank}"), "w") as f:
+            f.write(f"{int(ok_p)} {int(ok_s)}")
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("B,N,C", [(3, 17, 4), (2, 41, 5)])
+def test_time_sharded_viterbi_gloo_world2(tmp_path, B, N, C):
+    world = 2
+    mp.spawn(_vworker, args=(world, _free_port(), B, N, C, 5, str(tmp_path)), nprocs=world,
+             join=True)
+    for r in range(world):
+        assert open(tmp_path / f"v{r}").read() == "1 1", r

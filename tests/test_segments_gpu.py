@@ -102,3 +102,63 @@ def test_cfg5_generated_segments_sampled(dev):
             for e_i, e in enumerate(ed):
                 if begin <= e < begin + count:
                     check_marg(marg[b, e - begin].cpu().numpy(), m_ref[e_i])
+
+
+# ---------------------------------------------------------------- time-sharded Viterbi
+
+def virtual_viterbi(pot_np, G, dev):
+    """The time-sharded Viterbi flow (dist.time_sharded_viterbi) with the two all-gathers
+    replaced by device-side stacks; returns the stitched global path, scores, flags."""
+    B, E, C, _ = pot_np.shape
+    N = E + 1
+    segs = []
+    for r in range(G):
+        begin, count = tdist.shard_edges(E, G, r)
+        local = torch.from_numpy(np.ascontiguousarray(pot_np[:, begin:begin + count])).to(dev)
+        segs.append((begin, count, tsb.ViterbiSegment(local, begin, N)))
+    summ = torch.stack([s.summary() for (_, _, s) in segs])            # all_gather 1
+    res = [s.maps(summ, r, G) for r, (_, _, s) in enumerate(segs)]
+    maps = torch.stack([m for (m, _, _) in res])                        # all_gather 2
+    paths = [s.finish(maps, r, G) for r, (_, _, s) in enumerate(segs)]
+    torch.cuda.synchronize()
+    full = np.full((B, N), -2, np.int32)
+    for (begin, count, _), p in zip(segs, paths):
+        p = p.cpu().numpy()
+        seg_part = full[:, begin:begin + count + 1]
+        overlap = seg_part != -2
+        assert (seg_part[overlap] == p[overlap]).all()  # shared boundary nodes agree
+        full[:, begin:begin + count + 1] = p
+    scores = [sc.cpu().numpy() for (_, sc, _) in res]
+    flags = [fl.cpu().numpy() for (_, _, fl) in res]
+    return full, scores, flags
+
+
+@pytest.mark.parametrize("B,N,C,G", [(3, 257, 64, 2), (2, 1001, 128, 8), (3, 120, 20, 4),
+                                     (2, 50, 3, 8), (2, 9, 37, 8), (4, 64, 5, 3)])
+def test_virtual_viterbi_segments_bit_exact(dev, B, N, C, G):
+    pot = tsgen.potentials(B, N, C, seed=71 + G)
+    p_ref, s_ref, f_ref = oracle.chain_viterbi(pot, threads=8)
+    full, scores, flags = virtual_viterbi(pot, G, dev)
+    np.testing.assert_array_equal(full, p_ref)
+    for sc, fl in zip(scores, flags):
+        assert (sc == s_ref.astype(np.float32)).all()  # identical on every segment
+        assert (fl.astype(np.uint32) == f_ref).all()
+    # and equal to the unsharded GPU path
+    path, score, _ = tsb.viterbi(torch.from_numpy(pot).to(dev))
+    np.testing.assert_array_equal(path.cpu().numpy(), full)
+
+
+def test_virtual_viterbi_ties_and_flags(dev):
+    # coarse dyadic values: many exact ties (reading R5, smallest index wins)
+    B, N, C, G = 4, 80, 6, 4
+    pot = (np.random.default_rng(3).integers(-2, 3, size=(B, N - 1, C, C)) * 0.5).astype(np.float32)
+    pot[1] = -np.inf                                  # EMPTY
+    pot[2, 40, 1, 2] = np.nan                         # NONFINITE (in the 3rd segment)
+    p_ref, s_ref, f_ref = oracle.chain_viterbi(pot, threads=4)
+    full, scores, flags = virtual_viterbi(pot, G, dev)
+    for b in (0, 3):
+        np.testing.assert_array_equal(full[b], p_ref[b])
+        assert scores[0][b] == np.float32(s_ref[b])
+    assert (full[1] == -1).all() and (full[2] == -1).all()
+    for fl in flags:
+        assert (fl.astype(np.uint32) == f_ref).all()
