@@ -276,3 +276,57 @@ def ffbs_sample(pot, uniforms, lengths=None):
                 zz = _draw(al[t] + pot64[b, t, :, zz], u[k, b, t])
                 z[k, b, t] = zz
     return z
+
+
+def chain_kbest(pot, K: int, lengths=None):
+    """K-best labelings (Table 2 'K-Max'): the first K labelings of the total order
+    (Score descending, then reverse-lexicographic ascending — z_{n-1} first, the tie rule R5
+    extended), by the k-best max-plus DP written out in fp64:
+        delta_0[j] = [(0, -)],  delta_{t+1}[j] = top-K over (i, r) of delta_t[i][r] + l_t[i][j]
+    with candidates ordered by (score desc, i asc, r asc) — which is exactly the global order
+    restricted to partial paths ending at (t+1, j) — and the final merge over (score desc,
+    j asc, r asc).  -> (paths [B, K, N] int32 (-1 beyond len / missing), scores [B, K] f64
+    (-inf missing), flags [B])."""
+    pot64 = np.asarray(pot, dtype=np.float64)
+    B, E, C, _ = pot64.shape
+    N = E + 1
+    _, _, flags = chain_viterbi(pot, lengths)
+    paths = np.full((B, K, N), -1, dtype=np.int32)
+    scores = np.full((B, K), -math.inf, dtype=np.float64)
+    for b in range(B):
+        n = N if lengths is None else int(lengths[b])
+        if flags[b] & (F_NONFINITE | F_BADLEN):
+            scores[b, :] = math.nan
+            continue
+        # lists[j] = [(score, i, r)] sorted by (score desc, i asc, r asc); bps[t][j] = list
+        lists = [[(0.0, -1, -1)] for _ in range(C)]
+        bps = []
+        for t in range(n - 1):
+            new = []
+            for j in range(C):
+                cand = []
+                for i in range(C):
+                    lv = pot64[b, t, i, j]
+                    for r, (sc, _, _) in enumerate(lists[i]):
+                        v = sc + lv
+                        if v != -math.inf:
+                            cand.append((v, i, r))
+                cand.sort(key=lambda x: (-x[0], x[1], x[2]))
+                new.append(cand[:K])
+            bps.append(new)
+            lists = new
+        final = []
+        for j in range(C):
+            for r, (sc, _, _) in enumerate(lists[j]):
+                if sc != -math.inf:
+                    final.append((sc, j, r))
+        final.sort(key=lambda x: (-x[0], x[1], x[2]))
+        for q, (sc, j, r) in enumerate(final[:K]):
+            scores[b, q] = sc
+            z, slot = j, r
+            paths[b, q, n - 1] = z
+            for t in range(n - 2, -1, -1):
+                _, i, rr = bps[t][z][slot]
+                paths[b, q, t] = i
+                z, slot = i, rr
+    return paths, scores, flags

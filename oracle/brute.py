@@ -105,3 +105,14 @@ def entropy(pot_seq, n: int) -> float:
     _, p = probabilities(pot_seq, n)
     p = p[p > 0]
     return -math.fsum((p * np.log(p)).tolist())
+
+
+def kbest(pot_seq, n: int, K: int) -> tuple[np.ndarray, np.ndarray]:
+    """The first K labelings in the order (Score desc, then reverse-lexicographic asc:
+    z_{n-1} first) by sorting the enumeration — the definition of the K-Max result."""
+    Z, sc = scores(pot_seq, n)
+    keep = sc != -math.inf
+    Z, sc = Z[keep], sc[keep]
+    order = np.lexsort(tuple(Z.T) + (-sc,))  # last key first: -score, then z_{n-1}, ...
+    order = order[:K]
+    return Z[order].astype(np.int32), sc[order]

@@ -135,3 +135,50 @@ def test_ffbs_inverse_cdf_and_conditioning():
     pot2 = tsgen.potentials(2, N, C, seed=3)
     z2 = oracle.ffbs_sample(pot2, np.full((1, 2, N), 0.6), np.array([N, 1], np.int32))
     assert (z2[0, 1, 1:] == -1).all() and z2[0, 1, 0] == 2  # floor(0.6 * 4)
+
+
+# ---------------------------------------------------------------- f3: K-Max (k-best)
+
+@pytest.mark.parametrize("B,N,C,K", [(2, 4, 3, 5), (1, 5, 3, 243), (2, 3, 4, 7), (1, 1, 4, 6),
+                                     (2, 6, 2, 10)])
+def test_kbest_matches_enumeration(B, N, C, K):
+    # coarse dyadic values: many exact ties, so the tie order is exercised
+    pot = (np.random.default_rng(N * C + K).integers(-2, 3, size=(B, N - 1, C, C)) * 0.5
+           ).astype(np.float32)
+    paths, scores, flags = oracle.chain_kbest(pot, K)
+    for b in range(B):
+        Zr, sr = brute.kbest(pot[b], N, K)
+        m = len(sr)
+        np.testing.assert_array_equal(paths[b, :m], Zr)
+        np.testing.assert_array_equal(scores[b, :m], sr)
+        assert (scores[b, m:] == -np.inf).all() and (paths[b, m:] == -1).all()
+
+
+def test_kbest_k1_is_viterbi_and_zero_potentials():
+    pot = tsgen.potentials(3, 30, 6, seed=2, s=8)
+    paths, scores, _ = oracle.chain_kbest(pot, 1)
+    p_ref, s_ref, _ = oracle.chain_viterbi(pot)
+    np.testing.assert_array_equal(paths[:, 0], p_ref)
+    np.testing.assert_array_equal(scores[:, 0], s_ref)
+    # l = 0: every labelling scores 0; the order is reverse-lexicographic (z_{n-1} most
+    # significant), so the q-th labelling is q written in base C with z_0 the lowest digit
+    N, C, K = 4, 3, 10
+    paths, scores, _ = oracle.chain_kbest(np.zeros((1, N - 1, C, C), np.float32), K)
+    assert (scores == 0).all()
+    q = np.arange(K)
+    ref = np.stack([(q // C ** p) % C for p in range(N)], axis=1)
+    np.testing.assert_array_equal(paths[0], ref)
+
+
+def test_kbest_lengths_and_flags():
+    pot = tsgen.potentials(4, 6, 3, seed=5, s=8)
+    pot[2] = -np.inf
+    pot[3, 1, 0, 0] = np.nan
+    lengths = np.array([6, 2, 6, 6], np.int32)
+    paths, scores, flags = oracle.chain_kbest(pot, 4, lengths)
+    Zr, sr = brute.kbest(pot[1], 2, 4)
+    np.testing.assert_array_equal(paths[1, :, :2], Zr)
+    assert (paths[1, :, 2:] == -1).all()
+    assert (scores[2] == -np.inf).all() and (paths[2] == -1).all()
+    assert np.isnan(scores[3]).all() and (paths[3] == -1).all()
+    assert flags[2] == oracle.F_EMPTY and flags[3] == oracle.F_NONFINITE
