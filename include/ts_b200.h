@@ -79,7 +79,8 @@ enum {
   TS_OP_SEGMENT = 4,   /* ts_segment_summary + ts_segment_finish            */
   TS_OP_ENTROPY = 5,   /* ts_entropy (TS_LOG)                               */
   TS_OP_SAMPLE = 6,    /* ts_sample (TS_LOG, C <= 128)                      */
-  TS_OP_SEGMENT_VITERBI = 7 /* ts_segment_viterbi_maps + _finish (same ws)   */
+  TS_OP_SEGMENT_VITERBI = 7, /* ts_segment_viterbi_maps + _finish (same ws)  */
+  TS_OP_KBEST = 8      /* ts_kbest: size via ts_kbest_workspace_bytes(c, K)  */
 };
 
 /* One batch of chains.  N >= 1 positions (N-1 edges), 1 <= B, 1 <= C <= 256.
@@ -113,6 +114,18 @@ TS_API ts_status ts_marginals(const ts_chain *c, ts_semiring s, float *marg, flo
  * path [B][N] int32 out (-1 beyond len_b); score [B] fp32 out; flags [B] out or NULL. */
 TS_API ts_status ts_viterbi(const ts_chain *c, int32_t *path, float *score, uint32_t *flags,
                             void *ws, size_t ws_bytes, void *stream);
+
+/* ---- K-best Viterbi (Table 2 'K-Max') ---------------------------
+ * The first K labelings (1 <= K <= 16) of the order: Score descending, then reverse-
+ * lexicographic ascending (z_{len-1} compared first — reading R5 extended, R16),
+ * by the k-best max-plus recursion with backpointers.  paths [B][K][N] int32 out (-1 beyond
+ * len, for missing entries when fewer than K labelings have a finite score, and for flagged
+ * sequences); scores [B][K] fp32 out (-inf missing, NaN flagged); flags [B] or NULL.
+ * Bit-identical to the fp64 oracle on inputs whose path sums are exact in fp32.
+ * ws: ts_kbest_workspace_bytes(c, K) bytes (backpointers), 256-byte aligned. */
+TS_API size_t ts_kbest_workspace_bytes(const ts_chain *c, int64_t K);
+TS_API ts_status ts_kbest(const ts_chain *c, int64_t K, int32_t *paths, float *scores,
+                          uint32_t *flags, void *ws, size_t ws_bytes, void *stream);
 
 /* ---- time-sharded Viterbi (the max-plus form of the §6(a) scan,
  * P:307-311, across devices; Table 2 'Max' P:200; tie rule R5) -------------------

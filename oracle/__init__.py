@@ -281,7 +281,7 @@ def ffbs_sample(pot, uniforms, lengths=None):
 def chain_kbest(pot, K: int, lengths=None):
     """K-best labelings (Table 2 'K-Max'): the first K labelings of the total order
     (Score descending, then reverse-lexicographic ascending — z_{n-1} first, the tie rule R5
-    extended), by the k-best max-plus DP written out in fp64:
+    extended; reading R16), by the k-best max-plus DP written out in fp64:
         delta_0[j] = [(0, -)],  delta_{t+1}[j] = top-K over (i, r) of delta_t[i][r] + l_t[i][j]
     with candidates ordered by (score desc, i asc, r asc) — which is exactly the global order
     restricted to partial paths ending at (t+1, j) — and the final merge over (score desc,

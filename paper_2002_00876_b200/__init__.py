@@ -317,6 +317,22 @@ class Segment:
         return marg, logz, flags
 
 
+def kbest(pot: torch.Tensor, K: int, lengths=None, ws: Workspace | None = None):
+    """The K best labelings (Table 2 'K-Max'; order: score desc, then reverse-
+    lexicographic): (paths [B, K, N] int32, scores [B, K], flags [B])."""
+    L = _lib.load()
+    ch = _chain(pot, lengths)
+    B, E = pot.shape[0], pot.shape[1]
+    paths = torch.empty((B, K, E + 1), dtype=torch.int32, device=pot.device)
+    scores = torch.empty((B, K), dtype=torch.float32, device=pot.device)
+    flags = torch.empty(B, dtype=torch.int32, device=pot.device)
+    need = int(L.ts_kbest_workspace_bytes(ctypes.byref(ch), int(K)))
+    ws = ws or Workspace.get(pot.device)
+    _lib.check(L.ts_kbest(ctypes.byref(ch), int(K), paths.data_ptr(), scores.data_ptr(),
+                          flags.data_ptr(), ws.ptr(need), need, _stream(pot.device)), "ts_kbest")
+    return paths, scores, flags
+
+
 class ViterbiSegment:
     """One rank's contiguous time segment for time-sharded Viterbi: the
     max-plus summary, then (after gathering every rank's summary) the end-label maps, then

@@ -13,7 +13,7 @@ LIB_PATH = os.path.join(_HERE, "libts_b200.so")
 
 TS_LOG, TS_MAX = 0, 1
 TS_OP_LOGZ, TS_OP_MARG, TS_OP_VITERBI, TS_OP_MARG_HOST, TS_OP_SEGMENT = 0, 1, 2, 3, 4
-TS_OP_ENTROPY, TS_OP_SAMPLE, TS_OP_SEGMENT_VITERBI = 5, 6, 7
+TS_OP_ENTROPY, TS_OP_SAMPLE, TS_OP_SEGMENT_VITERBI, TS_OP_KBEST = 5, 6, 7, 8
 TS_F_EMPTY, TS_F_NONFINITE, TS_F_BADLEN = 1, 2, 4
 STATUS = {0: "TS_OK", 1: "TS_E_INVALID", 2: "TS_E_UNSUPPORTED", 3: "TS_E_WORKSPACE",
           4: "TS_E_CUDA"}
@@ -25,6 +25,7 @@ SYMBOLS = ("ts_workspace_bytes", "ts_logpartition", "ts_marginals", "ts_viterbi"
            "ts_set_tiny", "ts_entropy", "ts_log_prob", "ts_sample",
            "ts_segment_viterbi_summary_bytes", "ts_segment_viterbi_summary",
            "ts_segment_viterbi_maps", "ts_segment_viterbi_finish",
+           "ts_kbest_workspace_bytes", "ts_kbest",
            "ts_set_meet", "ts_set_viterbi_split", "ts_set_host_graphs",
            "ts_host_alloc", "ts_host_free", "ts_set_tc_summary", "ts_get_tc_summary",
            "ts_last_launch_count", "ts_last_kernel", "ts_status_str", "ts_version")
@@ -67,6 +68,9 @@ def load():
     L.ts_segment_summary.argtypes = [CH, I64, I64, INT, P, P, SZ, P]
     L.ts_segment_finish.argtypes = [CH, I64, I64, INT, INT, INT, P, P, P, P, P, SZ, P]
     L.ts_entropy.argtypes = [CH, P, P, P, P, P, SZ, P]
+    L.ts_kbest_workspace_bytes.argtypes = [CH, I64]
+    L.ts_kbest_workspace_bytes.restype = SZ
+    L.ts_kbest.argtypes = [CH, I64, P, P, P, P, SZ, P]
     L.ts_segment_viterbi_summary_bytes.argtypes = [CH]
     L.ts_segment_viterbi_summary_bytes.restype = SZ
     L.ts_segment_viterbi_summary.argtypes = [CH, I64, I64, P, P]
@@ -77,7 +81,7 @@ def load():
     for f in ("ts_logpartition", "ts_marginals", "ts_viterbi", "ts_marginals_host",
               "ts_segment_summary", "ts_segment_finish", "ts_entropy", "ts_log_prob",
               "ts_sample", "ts_segment_viterbi_summary", "ts_segment_viterbi_maps",
-              "ts_segment_viterbi_finish"):
+              "ts_segment_viterbi_finish", "ts_kbest"):
         getattr(L, f).restype = INT
     L.ts_set_plan_chunk.argtypes = [I64]
     L.ts_set_plan_chunk.restype = None

@@ -593,11 +593,45 @@ TS_API size_t ts_workspace_bytes(const ts_chain* c, int op, ts_semiring s) {
     if (c->C > 128) return 0;
     return stream_ws(c, seg_plan(c), true, nullptr, nullptr, nullptr, true);
   }
+  if (op == TS_OP_KBEST) return 0;  // use ts_kbest_workspace_bytes (depends on K)
   if (op == TS_OP_SEGMENT_VITERBI) return c->C <= 128 ? vseg_ws(c, nullptr, nullptr) : 0;
   if (op == TS_OP_ENTROPY) return s == TS_LOG ? entropy_ws(c, nullptr, nullptr, nullptr) : 0;
   if (op == TS_OP_SAMPLE) return (s == TS_LOG && c->C <= 128) ? sample_ws(c, nullptr, nullptr, nullptr) : 0;
   if (op < TS_OP_LOGZ || op > TS_OP_VITERBI) return 0;
   return op_ws(c, op, s, nullptr, nullptr, nullptr);
+}
+
+TS_API size_t ts_kbest_workspace_bytes(const ts_chain* c, int64_t K) {
+  if (!chain_ok(c) || K < 1 || K > 16) return 0;
+  const int64_t E = c->N - 1 > 0 ? c->N - 1 : 1;
+  return align_up(sizeof(uint16_t) * (size_t)(c->B * E * c->C * kbest_km(K)));
+}
+
+TS_API ts_status ts_kbest(const ts_chain* c, int64_t K, int32_t* paths, float* scores,
+                          uint32_t* flags, void* ws, size_t ws_bytes, void* stream) {
+  if (!chain_ok(c) || K < 1 || K > 16 || !paths || !aligned(paths, 4) || !scores ||
+      !aligned(scores, 4) || (flags && !aligned(flags, 4)))
+    return TS_E_INVALID;
+  if (!device_ok()) return TS_E_UNSUPPORTED;
+  const size_t need = ts_kbest_workspace_bytes(c, K);
+  if (ws_bytes < need || !ws || !aligned(ws, kAlign)) return TS_E_WORKSPACE;
+  KbestArgs a{};
+  a.pot = c->pot;
+  a.lengths = c->lengths;
+  a.B = c->B;
+  a.N = c->N;
+  a.C = c->C;
+  a.K = K;
+  a.bp = static_cast<uint16_t*>(ws);
+  a.paths = paths;
+  a.scores = scores;
+  a.flags = flags;
+  ts_status r = cuda_status(launch_kbest(a, static_cast<cudaStream_t>(stream)));
+  if (r == TS_OK) {
+    t_launches = 1;
+    t_kernel = "kbest_kernel";
+  }
+  return r;
 }
 
 TS_API size_t ts_segment_viterbi_summary_bytes(const ts_chain* local) {

@@ -1,0 +1,196 @@
+// kbest.cu — K-best Viterbi (Table 2 'K-Max' semiring).
+//
+// delta_{t+1}[j] = the top-KM (score, i, r) of delta_t[i][r] + l_t[i][j] over all labels i and
+// ranks r, ordered by (score desc, i asc, r asc); delta_0[j] = [(0)].  That order is the
+// global order of DESIGN.md reading R16 (Score desc, then reverse-lexicographic asc)
+// restricted to partial paths ending at (t+1, j), so the final merge over (score desc,
+// j asc, r asc) yields the first K labelings of that order.  KM = the next power of two
+// >= K (keeping more candidates than K never changes the top K).  fp32 sums of dyadic
+// inputs are exact, so the result equals the fp64 oracle bit for bit.
+//
+// One CTA per sequence, thread j owns column j and keeps its sorted list in registers;
+// lists live in SMEM between steps; backpointers (i | r << 8) as uint16 [B][E][C][KM].
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace tsb {
+
+template <int KM>
+__global__ void __launch_bounds__(256) kbest_kernel(KbestArgs a) {
+  extern __shared__ __align__(16) float ksm[];
+  const int C = (int)a.C;
+  const int64_t N = a.N, E = N - 1, CC = (int64_t)C * C;
+  const int64_t b = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, NW = blockDim.x >> 5;
+  const bool act = tid < C;
+  float* dl = ksm;                                  // [2][C][KM]
+  float* rs = dl + 2 * (size_t)C * KM;              // [NW] block-reduction scores
+  int* ri = reinterpret_cast<int*>(rs + NW);        // [NW] block-reduction labels
+  int* sel = ri + NW;                               // [K][2] final (j, r)
+  unsigned* bad = reinterpret_cast<unsigned*>(sel + 2 * a.K);
+  const int K = (int)a.K;
+  int32_t* pb = a.paths + b * (int64_t)K * N;
+  float* sb = a.scores + b * K;
+  const int64_t len = seq_len(a.lengths, b, N);
+  if (len < 0) {
+    for (int64_t q = tid; q < (int64_t)K * N; q += blockDim.x) pb[q] = -1;
+    for (int q = tid; q < K; q += blockDim.x) sb[q] = qnan();
+    if (tid == 0 && a.flags) a.flags[b] = TS_F_BADLEN;
+    return;
+  }
+  const int64_t Eb = len - 1;
+  if (tid == 0) *bad = 0u;
+  if (act) {
+#pragma unroll
+    for (int r = 0; r < KM; ++r) dl[tid * KM + r] = (r == 0) ? 0.f : neg_inf();
+  }
+  __syncthreads();
+  float sc[KM];
+  int ii[KM], rr[KM];
+  int cur = 0;
+  bool nonfin = false;
+  for (int64_t t = 0; t < Eb; ++t) {
+#pragma unroll
+    for (int r = 0; r < KM; ++r) {
+      sc[r] = neg_inf();
+      ii[r] = 0;
+      rr[r] = 0;
+    }
+    const float* d = dl + (size_t)cur * C * KM;
+    if (act) {
+      const float* col = a.pot + (b * E + t) * CC + tid;
+      for (int i = 0; i < C; ++i) {
+        const float lv = col[(int64_t)i * C];
+        nonfin |= (lv != lv) | (lv == pos_inf());
+        if (lv == neg_inf()) continue;
+        for (int r = 0; r < KM; ++r) {
+          const float v = d[i * KM + r] + lv;
+          if (!(v > sc[KM - 1])) break;  // lists are sorted: no later r can enter
+          int pos = 0;
+#pragma unroll
+          for (int q = 0; q < KM; ++q) pos += (sc[q] >= v) ? 1 : 0;
+#pragma unroll
+          for (int p = KM - 1; p > 0; --p)
+            if (p > pos) {
+              sc[p] = sc[p - 1];
+              ii[p] = ii[p - 1];
+              rr[p] = rr[p - 1];
+            }
+#pragma unroll
+          for (int p = 0; p < KM; ++p)
+            if (p == pos) {
+              sc[p] = v;
+              ii[p] = i;
+              rr[p] = r;
+            }
+        }
+      }
+      float* dn = dl + (size_t)(cur ^ 1) * C * KM + (size_t)tid * KM;
+      uint16_t* bpo = a.bp + ((b * E + t) * C + tid) * KM;
+#pragma unroll
+      for (int r = 0; r < KM; ++r) {
+        dn[r] = sc[r];
+        bpo[r] = (uint16_t)(ii[r] | (rr[r] << 8));
+      }
+    }
+    cur ^= 1;
+    __syncthreads();
+  }
+  if (__any_sync(0xffffffffu, nonfin) && lane == 0) atomicOr(bad, 1u);
+  // final merge over (score desc, j asc, r asc): K rounds of a block arg-max over list heads
+  const float* d = dl + (size_t)cur * C * KM;
+  int h = 0;
+  for (int q = 0; q < K; ++q) {
+    float v = (act && h < KM) ? d[tid * KM + h] : neg_inf();
+    int idx = (act && v != neg_inf()) ? tid : 0x7fffffff;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, v, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+      if (ov > v || (ov == v && oi < idx)) {
+        v = ov;
+        idx = oi;
+      }
+    }
+    if (lane == 0) {
+      rs[w] = v;
+      ri[w] = idx;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      float bv = rs[0];
+      int bi = ri[0];
+      for (int k = 1; k < NW; ++k)
+        if (rs[k] > bv || (rs[k] == bv && ri[k] < bi)) {
+          bv = rs[k];
+          bi = ri[k];
+        }
+      sb[q] = bv;
+      sel[2 * q] = (bv == neg_inf()) ? -1 : bi;
+      sel[2 * q + 1] = -1;
+      rs[0] = bv;
+      ri[0] = bi;
+    }
+    __syncthreads();
+    if (rs[0] != neg_inf() && tid == ri[0]) {  // the winner reports its rank and advances
+      sel[2 * q + 1] = h;
+      ++h;
+    }
+    __syncthreads();
+  }
+  const bool nf = *bad != 0u;
+  if (tid == 0 && a.flags) {
+    const bool empty = !nf && (K > 0) && sb[0] == neg_inf();
+    a.flags[b] = nf ? (unsigned)TS_F_NONFINITE : (empty ? (unsigned)TS_F_EMPTY : 0u);
+  }
+  // backtrack: thread q < K walks its path back through the backpointers
+  if (tid < K) {
+    const int q = tid;
+    int32_t* pq = pb + (int64_t)q * N;
+    int z = sel[2 * q], slot = sel[2 * q + 1];
+    if (nf) {
+      sb[q] = qnan();
+      z = -1;
+    }
+    for (int64_t n = len; n < N; ++n) pq[n] = -1;
+    if (z < 0 || slot < 0) {
+      for (int64_t n = 0; n < len; ++n) pq[n] = -1;
+    } else {
+      pq[Eb] = z;
+      for (int64_t t = Eb - 1; t >= 0; --t) {
+        const uint16_t v = a.bp[((b * E + t) * C + z) * KM + slot];
+        z = v & 0xFF;
+        slot = v >> 8;
+        pq[t] = z;
+      }
+    }
+  }
+}
+
+int kbest_km(int64_t K) {
+  int km = 1;
+  while (km < K) km <<= 1;
+  return km;
+}
+
+size_t kbest_smem(int64_t C, int64_t K) {
+  const int km = kbest_km(K);
+  return (2 * (size_t)C * km + 8) * sizeof(float) + 8 * sizeof(int) + 2 * (size_t)K * sizeof(int) + 16;
+}
+
+cudaError_t launch_kbest(const KbestArgs& a, cudaStream_t st) {
+  const int km = kbest_km(a.K);
+  const int NT = (int)(((a.C + 31) / 32) * 32);
+  const size_t smem = kbest_smem(a.C, a.K);
+  switch (km) {
+    case 1: kbest_kernel<1><<<(unsigned)a.B, NT, smem, st>>>(a); break;
+    case 2: kbest_kernel<2><<<(unsigned)a.B, NT, smem, st>>>(a); break;
+    case 4: kbest_kernel<4><<<(unsigned)a.B, NT, smem, st>>>(a); break;
+    case 8: kbest_kernel<8><<<(unsigned)a.B, NT, smem, st>>>(a); break;
+    case 16: kbest_kernel<16><<<(unsigned)a.B, NT, smem, st>>>(a); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace tsb

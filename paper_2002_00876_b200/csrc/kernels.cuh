@@ -175,6 +175,20 @@ cudaError_t launch_entropy(DistArgs a, cudaStream_t st);
 cudaError_t launch_score(const DistArgs& a, cudaStream_t st);
 cudaError_t launch_sample(const DistArgs& a, cudaStream_t st);
 
+// ---- K-best Viterbi (kbest.cu) -------------------------------------------
+struct KbestArgs {
+  const float* pot;
+  const int32_t* lengths;
+  int64_t B, N, C, K;
+  uint16_t* bp;      // [B][N-1][C][KM] (i | r << 8)
+  int32_t* paths;    // [B][K][N]
+  float* scores;     // [B][K]
+  uint32_t* flags;   // [B] or nullptr
+};
+int kbest_km(int64_t K);
+size_t kbest_smem(int64_t C, int64_t K);
+cudaError_t launch_kbest(const KbestArgs& a, cudaStream_t st);
+
 // ---- time-sharded Viterbi segments (vseg.cu) -------------------------------
 struct VsegArgs {
   const float* pot;       // local edges [B][E_loc][C][C]
