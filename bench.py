@@ -170,6 +170,8 @@ def main():
     ap.add_argument("--sets", type=int, default=0, help="rotating buffer sets (0 = auto > 2x L2)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=0)
+    ap.add_argument("--tiny-mode", type=int, default=-1,
+                    help="debug: cfg2 kernel variant (ts_set_tiny: 1 default, 2 overlapped)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -181,6 +183,8 @@ def main():
     import tsgen
 
     rank, local_rank, world = env_rank()
+    if args.tiny_mode >= 0:
+        tsb.set_tiny(args.tiny_mode)
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     dist = None
