@@ -330,3 +330,73 @@ def chain_kbest(pot, K: int, lengths=None):
                 paths[b, q, t] = i
                 z, slot = i, rr
     return paths, scores, flags
+
+
+# ---------------------------------------------------------------------------------------
+# semi-Markov CRF on the same chain machinery (Table 1 'Semi-Markov',
+# P:44; "similar parallel approach can also be used for ... semi-Markov").
+# Reading R17: pot [B, N-1, K, C, C]; l[b, n, k-1, c1, c2] scores a segment that
+# covers the k steps n -> n+k with label c2, following label c1 at node n.  A labelled
+# segmentation is 0 = p_0 < p_1 < ... < p_m = E_b (E_b = len_b - 1, p_s - p_{s-1} <= K) with
+# labels y_0 (free) ... y_m; Score = Σ_s l[p_{s-1}, p_s - p_{s-1} - 1, y_{s-1}, y_s].
+# K = 1 is exactly the linear chain.
+# ---------------------------------------------------------------------------------------
+
+def _lse_np(x, axis=None):
+    m = np.max(x, axis=axis, keepdims=True)
+    mf = np.where(np.isfinite(m), m, 0.0)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        r = np.log(np.sum(np.exp(x - mf), axis=axis, keepdims=True)) + mf
+    r = np.where(np.isfinite(m), r, m)
+    return np.squeeze(r, axis=axis) if axis is not None else float(r.reshape(()))
+
+
+def semimarkov_marginals(pot, lengths=None, want_marg: bool = True):
+    """Segmental forward-backward in fp64 (the per-cell max of §6(c) via LSE):
+        alpha_0 = 0, alpha_p[c] = LSE_{k<=min(K,p), c'} alpha_{p-k}[c'] + l[p-k, k-1, c', c]
+        beta_E  = 0, beta_p[c]  = LSE_{k<=min(K,E-p), c'} l[p, k-1, c, c'] + beta_{p+k}[c']
+        A = LSE_c alpha_E[c],   mu[n,k-1,c1,c2] = exp(alpha_n[c1] + l + beta_{n+k}[c2] - A)
+    Flags as chain_marginals (EMPTY: A = -inf -> mu = 0; NaN/+inf on a used part ->
+    NONFINITE, A = NaN; bad length -> BADLEN).  -> (logz [B], marg [B,N-1,K,C,C] | None, flags)."""
+    pot64 = np.asarray(pot, dtype=np.float64)
+    B, E, K, C, _ = pot64.shape
+    N = E + 1
+    logz = np.empty(B)
+    marg = np.zeros(pot64.shape) if want_marg else None
+    flags = np.zeros(B, dtype=np.uint32)
+    for b in range(B):
+        n_b = N if lengths is None else int(lengths[b])
+        if n_b < 1 or n_b > N:
+            logz[b] = math.nan
+            flags[b] = F_BADLEN
+            continue
+        Eb = n_b - 1
+        used = np.zeros((E, K), bool)
+        for n in range(Eb):
+            used[n, :min(K, Eb - n)] = True
+        if np.any(~np.isfinite(pot64[b][used]) & ~(pot64[b][used] == -np.inf)):
+            logz[b] = math.nan
+            flags[b] = F_NONFINITE
+            continue
+        al = np.full((Eb + 1, C), -np.inf)
+        al[0] = 0.0
+        for p in range(1, Eb + 1):
+            terms = [al[p - k][:, None] + pot64[b, p - k, k - 1] for k in range(1, min(K, p) + 1)]
+            al[p] = _lse_np(np.concatenate(terms, axis=0), axis=0)
+        be = np.full((Eb + 1, C), -np.inf)
+        be[Eb] = 0.0
+        for p in range(Eb - 1, -1, -1):
+            terms = [pot64[b, p, k - 1] + be[p + k][None, :] for k in range(1, min(K, Eb - p) + 1)]
+            be[p] = _lse_np(np.concatenate(terms, axis=1), axis=1)
+        A = _lse_np(al[Eb])
+        logz[b] = A
+        if A == -np.inf:
+            flags[b] = F_EMPTY
+            continue
+        if want_marg:
+            for n in range(Eb):
+                for k in range(1, min(K, Eb - n) + 1):
+                    with np.errstate(invalid="ignore"):
+                        x = al[n][:, None] + pot64[b, n, k - 1] + be[n + k][None, :] - A
+                    marg[b, n, k - 1] = np.where(np.isfinite(x), np.exp(x), 0.0)
+    return logz, marg, flags

@@ -116,3 +116,48 @@ def kbest(pot_seq, n: int, K: int) -> tuple[np.ndarray, np.ndarray]:
     order = np.lexsort(tuple(Z.T) + (-sc,))  # last key first: -score, then z_{n-1}, ...
     order = order[:K]
     return Z[order].astype(np.int32), sc[order]
+
+
+def segmentations(E: int, K: int):
+    """All boundary sequences 0 = p_0 < ... < p_m = E with steps <= K (compositions of E)."""
+    out = []
+
+    def rec(p, acc):
+        if p == E:
+            out.append(list(acc))
+            return
+        for k in range(1, min(K, E - p) + 1):
+            acc.append(p + k)
+            rec(p + k, acc)
+            acc.pop()
+
+    rec(0, [0])
+    return out
+
+
+def semimarkov(pot_seq, n: int):
+    """(A, mu) of a semi-Markov chain by enumerating every segmentation x labelling (reading
+    R17): Score = Σ_s l[p_{s-1}, p_s - p_{s-1} - 1, y_{s-1}, y_s]."""
+    pot = np.asarray(pot_seq, dtype=np.float64)
+    _, K, C, _ = pot.shape
+    E = n - 1
+    items = []
+    for seg in segmentations(E, K):
+        m = len(seg) - 1
+        for ys in np.ndindex(*([C] * (m + 1))):
+            sc = 0.0
+            parts = []
+            for s in range(1, m + 1):
+                n0, k = seg[s - 1], seg[s] - seg[s - 1]
+                sc += pot[n0, k - 1, ys[s - 1], ys[s]]
+                parts.append((n0, k - 1, ys[s - 1], ys[s]))
+            items.append((sc, parts))
+    scs = np.array([it[0] for it in items])
+    A = _lse(scs)
+    mu = np.zeros(pot.shape)
+    if A != -math.inf:
+        for sc, parts in items:
+            w = math.exp(sc - A)
+            for q in parts:
+                mu[q] += w
+    return A, mu

@@ -182,3 +182,63 @@ def test_kbest_lengths_and_flags():
     assert (scores[2] == -np.inf).all() and (paths[2] == -1).all()
     assert np.isnan(scores[3]).all() and (paths[3] == -1).all()
     assert flags[2] == oracle.F_EMPTY and flags[3] == oracle.F_NONFINITE
+
+
+# ---------------------------------------------------------------- f4: semi-Markov (R17)
+
+@pytest.mark.parametrize("N,K,C", [(5, 2, 2), (4, 3, 3), (6, 3, 2), (3, 1, 3), (5, 4, 2), (1, 2, 3)])
+def test_semimarkov_matches_enumeration(N, K, C):
+    rng = np.random.default_rng(N * 100 + K * 10 + C)
+    pot = (rng.integers(-64, 65, size=(2, max(N - 1, 0), K, C, C)) / 32.0).astype(np.float32)
+    logz, marg, flags = oracle.semimarkov_marginals(pot)
+    assert (flags == 0).all()
+    for b in range(2):
+        A, mu = brute.semimarkov(pot[b], N)
+        assert abs(logz[b] - A) <= 1e-12 * max(1.0, abs(A))
+        np.testing.assert_allclose(marg[b], mu, rtol=0, atol=1e-12)
+
+
+def test_semimarkov_k1_is_the_linear_chain():
+    pot = tsgen.potentials(3, 20, 5, seed=8)
+    lz, mg, _ = oracle.chain_marginals(pot)
+    lz2, mg2, _ = oracle.semimarkov_marginals(pot[:, :, None, :, :])
+    np.testing.assert_allclose(lz2, lz, rtol=1e-13)
+    np.testing.assert_allclose(mg2[:, :, 0], mg, atol=1e-13)
+
+
+def test_semimarkov_count_compositions_and_coverage():
+    # C = 1, l = 0: A = log(#compositions of E into parts <= K) (E=4, K=2 -> 5)
+    for (E, K, cnt) in [(4, 2, 5), (3, 3, 4), (10, 3, 274)]:
+        lz, _, _ = oracle.semimarkov_marginals(np.zeros((1, E, K, 1, 1), np.float32))
+        assert lz[0] == pytest.approx(math.log(cnt), rel=1e-13)
+    # every step is covered by exactly one segment: Σ mu * k = E_b
+    pot = (np.random.default_rng(4).standard_normal((2, 12, 4, 3, 3))).astype(np.float32)
+    lengths = np.array([13, 7], np.int32)
+    _, mu, _ = oracle.semimarkov_marginals(pot, lengths)
+    ks = np.arange(1, 5)[None, None, :, None, None]
+    for b in range(2):
+        assert float((mu[b] * ks[0]).sum()) == pytest.approx(lengths[b] - 1, rel=1e-12)
+
+
+def test_semimarkov_finite_differences_and_flags():
+    pot = (np.random.default_rng(5).standard_normal((1, 6, 3, 2, 2))).astype(np.float64)
+    _, mu, _ = oracle.semimarkov_marginals(pot)
+    h = 2.0 ** -13
+    rng = np.random.default_rng(6)
+    for _ in range(8):
+        q = tuple(rng.integers(0, s) for s in pot.shape)
+        if q[1] + q[2] + 1 > 6:
+            continue
+        pp, pm = pot.copy(), pot.copy()
+        pp[q] += h
+        pm[q] -= h
+        fd = (oracle.semimarkov_marginals(pp, want_marg=False)[0][0] -
+              oracle.semimarkov_marginals(pm, want_marg=False)[0][0]) / (2 * h)
+        assert fd == pytest.approx(mu[q], abs=1e-7)
+    bad = (np.random.default_rng(7).standard_normal((3, 5, 2, 2, 2))).astype(np.float32)
+    bad[0] = -np.inf
+    bad[1, 1, 0, 1, 1] = np.nan
+    lz, mg, fl = oracle.semimarkov_marginals(bad)
+    assert fl[0] == oracle.F_EMPTY and lz[0] == -np.inf and (mg[0] == 0).all()
+    assert fl[1] == oracle.F_NONFINITE and math.isnan(lz[1])
+    assert fl[2] == 0
