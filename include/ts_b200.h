@@ -115,6 +115,18 @@ TS_API ts_status ts_marginals(const ts_chain *c, ts_semiring s, float *marg, flo
 TS_API ts_status ts_viterbi(const ts_chain *c, int32_t *path, float *score, uint32_t *flags,
                             void *ws, size_t ws_bytes, void *stream);
 
+/* ---- semi-Markov CRF (Table 1 'Semi-Markov') -------------
+ * Reading R17: c->pot is [B][N-1][K][C][C] fp32; l[b][n][k-1][c1][c2] scores a
+ * segment covering the k steps n -> n+k (1 <= k <= K <= 16) with label c2 after label c1
+ * at node n; a labelled segmentation of nodes 0 .. len-1 scores the sum of its segments.
+ * K = 1 is exactly the linear chain.  Segmental forward-backward (per-cell max, fp64
+ * offsets): logz [B] out (required); marg (same layout as pot, 0 for parts that end beyond
+ * the sequence) out or NULL; flags as ts_marginals.  C <= 128.
+ * ws: ts_semimarkov_workspace_bytes(c, K) bytes, 256-byte aligned. */
+TS_API size_t ts_semimarkov_workspace_bytes(const ts_chain *c, int64_t K);
+TS_API ts_status ts_semimarkov(const ts_chain *c, int64_t K, float *marg, float *logz,
+                               uint32_t *flags, void *ws, size_t ws_bytes, void *stream);
+
 /* ---- K-best Viterbi (Table 2 'K-Max') ---------------------------
  * The first K labelings (1 <= K <= 16) of the order: Score descending, then reverse-
  * lexicographic ascending (z_{len-1} compared first — reading R5 extended, R16),

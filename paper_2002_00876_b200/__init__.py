@@ -317,6 +317,26 @@ class Segment:
         return marg, logz, flags
 
 
+def semimarkov(pot: torch.Tensor, lengths=None, want_marg: bool = True,
+               ws: Workspace | None = None):
+    """Semi-Markov CRF (Table 1; reading R17): pot [B, N-1, K, C, C] ->
+    (marg (same shape) | None, logZ [B], flags [B])."""
+    L = _lib.load()
+    assert pot.dim() == 5 and pot.is_contiguous()
+    B, E, K, C, _ = pot.shape
+    ch = _lib.ts_chain(B, E + 1, C, pot.data_ptr(),
+                       lengths.data_ptr() if lengths is not None else None)
+    marg = torch.empty_like(pot) if want_marg else None
+    logz = torch.empty(B, dtype=torch.float32, device=pot.device)
+    flags = torch.empty(B, dtype=torch.int32, device=pot.device)
+    need = int(L.ts_semimarkov_workspace_bytes(ctypes.byref(ch), int(K)))
+    ws = ws or Workspace.get(pot.device)
+    _lib.check(L.ts_semimarkov(ctypes.byref(ch), int(K), marg.data_ptr() if want_marg else None,
+                               logz.data_ptr(), flags.data_ptr(), ws.ptr(need), need,
+                               _stream(pot.device)), "ts_semimarkov")
+    return marg, logz, flags
+
+
 def kbest(pot: torch.Tensor, K: int, lengths=None, ws: Workspace | None = None):
     """The K best labelings (Table 2 'K-Max'; order: score desc, then reverse-
     lexicographic): (paths [B, K, N] int32, scores [B, K], flags [B])."""

@@ -601,6 +601,52 @@ TS_API size_t ts_workspace_bytes(const ts_chain* c, int op, ts_semiring s) {
   return op_ws(c, op, s, nullptr, nullptr, nullptr);
 }
 
+TS_API size_t ts_semimarkov_workspace_bytes(const ts_chain* c, int64_t K) {
+  if (!chain_ok(c) || K < 1 || K > 16 || c->C > 128) return 0;
+  Carve cv(nullptr);
+  const int64_t B = c->B, N = c->N, C = c->C;
+  cv.take<float>((size_t)(B * N * C));
+  cv.take<float>((size_t)(B * N * C));
+  cv.take<double>((size_t)(B * N));
+  cv.take<double>((size_t)(B * N));
+  cv.take<double>((size_t)B);
+  return cv.off;
+}
+
+TS_API ts_status ts_semimarkov(const ts_chain* c, int64_t K, float* marg, float* logz,
+                               uint32_t* flags, void* ws, size_t ws_bytes, void* stream) {
+  if (!chain_ok(c) || K < 1 || K > 16 || !logz || !aligned(logz, 4) ||
+      (marg && !aligned(marg, 4)) || (flags && !aligned(flags, 4)))
+    return TS_E_INVALID;
+  if (c->C > 128) return TS_E_UNSUPPORTED;
+  if (!device_ok()) return TS_E_UNSUPPORTED;
+  const size_t need = ts_semimarkov_workspace_bytes(c, K);
+  if (ws_bytes < need || !ws || !aligned(ws, kAlign)) return TS_E_WORKSPACE;
+  Carve cv(ws);
+  const int64_t B = c->B, N = c->N, C = c->C;
+  SemiArgs a{};
+  a.pot = c->pot;
+  a.lengths = c->lengths;
+  a.B = B;
+  a.N = N;
+  a.C = C;
+  a.K = K;
+  a.marg = marg;
+  a.logz = logz;
+  a.flags = flags;
+  a.ah = cv.take<float>((size_t)(B * N * C));
+  a.bh = cv.take<float>((size_t)(B * N * C));
+  a.ao = cv.take<double>((size_t)(B * N));
+  a.bo = cv.take<double>((size_t)(B * N));
+  a.zbuf = cv.take<double>((size_t)B);
+  ts_status r = cuda_status(launch_semimarkov(a, static_cast<cudaStream_t>(stream)));
+  if (r == TS_OK) {
+    t_launches = 1;
+    t_kernel = "semimarkov_kernel";
+  }
+  return r;
+}
+
 TS_API size_t ts_kbest_workspace_bytes(const ts_chain* c, int64_t K) {
   if (!chain_ok(c) || K < 1 || K > 16) return 0;
   const int64_t E = c->N - 1 > 0 ? c->N - 1 : 1;

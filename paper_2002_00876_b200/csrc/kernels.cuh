@@ -175,6 +175,22 @@ cudaError_t launch_entropy(DistArgs a, cudaStream_t st);
 cudaError_t launch_score(const DistArgs& a, cudaStream_t st);
 cudaError_t launch_sample(const DistArgs& a, cudaStream_t st);
 
+// ---- semi-Markov CRF (semimarkov.cu, reading R17) -----------------------
+struct SemiArgs {
+  const float* pot;        // [B][N-1][K][C][C]
+  const int32_t* lengths;
+  int64_t B, N, C, K;
+  float* marg;             // same layout as pot, or nullptr
+  float* logz;
+  uint32_t* flags;
+  float* ah;               // [B][N][C] normalised forward vectors (workspace)
+  float* bh;               // [B][N][C] normalised backward vectors
+  double* ao;              // [B][N] natural offsets
+  double* bo;
+  double* zbuf;            // [B] logZ in fp64
+};
+cudaError_t launch_semimarkov(const SemiArgs& a, cudaStream_t st);
+
 // ---- K-best Viterbi (kbest.cu) -------------------------------------------
 struct KbestArgs {
   const float* pot;

@@ -1,0 +1,182 @@
+// semimarkov.cu — semi-Markov CRF log-partition and marginals (Table 1
+// 'Semi-Markov', "similar parallel approach ... semi-Markov", P:311;
+// reading R17: pot [B][N-1][K][C][C], l[b,n,k-1,c1,c2] scores a segment covering the k
+// steps n -> n+k with label c2 after label c1 at node n; K = 1 is the linear chain).
+//
+// Segmental forward-backward, one CTA per sequence: threads 0..127 run the forward
+// recursion (thread c), threads 128..255 the backward recursion concurrently:
+//   alpha_p[c] = LSE_{k <= min(K,p), c'} alpha_{p-k}[c'] + l[p-k, k-1, c', c]
+//   beta_p[c]  = LSE_{k <= min(K,E-p), c'} l[p, k-1, c, c'] + beta_{p+k}[c']
+// with the per-cell max of §6(c) and node vectors stored normalised (max 0) with
+// fp64 natural offsets (the last K+1 vectors also in an SMEM ring).  Then all threads write
+//   mu[n,k-1,c1,c2] = exp(alpha_n[c1] + l[n,k-1,c1,c2] + beta_{n+k}[c2] - A)
+// (0 for parts beyond the sequence).  Flags as the linear chain.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace tsb {
+
+namespace {
+constexpr int kSmG = 128;  // threads per recursion group (C <= 128)
+
+__device__ __forceinline__ float group_max(float v, float* red, int gw, int bar_id) {
+  v = warp_max(v);
+  if ((threadIdx.x & 31) == 0) red[gw] = v;
+  named_bar(bar_id, kSmG);
+  float r = red[0];
+  for (int k = 1; k < kSmG / 32; ++k) r = fmaxf(r, red[k]);
+  named_bar(bar_id, kSmG);
+  return r;
+}
+}  // namespace
+
+__global__ void __launch_bounds__(2 * kSmG) semimarkov_kernel(SemiArgs a) {
+  extern __shared__ __align__(16) float ssm[];
+  const int C = (int)a.C, K = (int)a.K;
+  const int64_t N = a.N, E = N - 1, KCC = (int64_t)K * C * C;
+  const int64_t b = blockIdx.x;
+  const int tid = threadIdx.x, grp = tid / kSmG, c = tid % kSmG, gw = c >> 5;
+  const int R = K + 1;                                   // ring rows
+  float* ring = ssm + grp * R * kSmG;                    // [2][R][128] normalised vectors
+  double* ooff = reinterpret_cast<double*>(ssm + 2 * R * kSmG) + grp * R;  // [2][R] offsets
+  float* red0 = reinterpret_cast<float*>(reinterpret_cast<double*>(ssm + 2 * R * kSmG) + 2 * R);
+  float* red = red0 + grp * 8;                           // [2][8] per-group reductions
+  unsigned* sflag = reinterpret_cast<unsigned*>(red0 + 16);  // one word for the CTA
+  const float* pb = a.pot + b * E * KCC;
+  float* mg = a.marg ? a.marg + b * E * KCC : nullptr;
+  const int64_t len = seq_len(a.lengths, b, N);
+  if (len < 0) {
+    if (mg)
+      for (int64_t q = tid; q < E * KCC; q += blockDim.x) mg[q] = 0.f;
+    if (tid == 0) {
+      a.logz[b] = qnan();
+      if (a.flags) a.flags[b] = TS_F_BADLEN;
+    }
+    return;
+  }
+  const int64_t Eb = len - 1;
+  if (tid == 0) *sflag = 0u;
+  __syncthreads();
+  const bool act = c < C;
+  float* vh = (grp == 0 ? a.ah : a.bh) + b * N * C;      // [N][C] normalised vectors
+  double* vo = (grp == 0 ? a.ao : a.bo) + b * N;         // [N] natural offsets
+  bool bad = false;
+  // node 0 (forward) / node Eb (backward): log-one vector, offset 0
+  {
+    const int64_t n0 = grp == 0 ? 0 : Eb;
+    ring[(n0 % R) * kSmG + c] = act ? 0.f : neg_inf();
+    if (act) vh[n0 * C + c] = 0.f;
+    if (c == 0) {
+      ooff[n0 % R] = 0.0;
+      vo[n0] = 0.0;
+    }
+  }
+  named_bar(1 + grp, kSmG);
+  for (int64_t s = 1; s <= Eb; ++s) {
+    const int64_t p = grp == 0 ? s : Eb - s;             // node computed at this step
+    const int64_t pr = grp == 0 ? p - 1 : p + 1;         // reference node (offset frame)
+    const int kmax = (int)(grp == 0 ? (p < K ? p : K) : (Eb - p < K ? Eb - p : K));
+    const double oref = ooff[pr % R];
+    float m = neg_inf();
+    for (int k = 1; k <= kmax; ++k) {
+      const int64_t q = grp == 0 ? p - k : p + k;        // the other end of the segment
+      const float d = (float)(ooff[q % R] - oref);
+      const float* vq = ring + (q % R) * kSmG;
+      const float* lt = grp == 0 ? pb + (p - k) * KCC + (int64_t)(k - 1) * C * C
+                                 : pb + p * KCC + (int64_t)(k - 1) * C * C;
+      if (act)
+        for (int c2 = 0; c2 < C; ++c2) {
+          const float lv = grp == 0 ? lt[(int64_t)c2 * C + c] : lt[(int64_t)c * C + c2];
+          bad |= (lv != lv) | (lv == pos_inf());
+          m = fmaxf(m, d + vq[c2] + lv);
+        }
+    }
+    float sum = 0.f;
+    if (act && m != neg_inf())
+      for (int k = 1; k <= kmax; ++k) {
+        const int64_t q = grp == 0 ? p - k : p + k;
+        const float d = (float)(ooff[q % R] - oref);
+        const float* vq = ring + (q % R) * kSmG;
+        const float* lt = grp == 0 ? pb + (p - k) * KCC + (int64_t)(k - 1) * C * C
+                                   : pb + p * KCC + (int64_t)(k - 1) * C * C;
+        for (int c2 = 0; c2 < C; ++c2) {
+          const float lv = grp == 0 ? lt[(int64_t)c2 * C + c] : lt[(int64_t)c * C + c2];
+          sum += ex2((d + vq[c2] + lv - m) * kLog2e);
+        }
+      }
+    const float val = (act && m != neg_inf()) ? m + lg2(sum) * (float)kLn2 : neg_inf();
+    const float M = group_max(val, red, gw, 1 + grp);
+    const bool dead = (M == neg_inf());
+    const float nv = (act && !dead) ? val - M : neg_inf();
+    ring[(p % R) * kSmG + c] = nv;
+    if (act) vh[p * C + c] = nv;
+    if (c == 0) {
+      const double o = dead ? oref : oref + (double)M;
+      ooff[p % R] = o;
+      vo[p] = dead ? -INFINITY : o;
+    }
+    named_bar(1 + grp, kSmG);
+  }
+  if (__any_sync(0xffffffffu, bad) && (tid & 31) == 0) atomicOr(sflag, (unsigned)TS_F_NONFINITE);
+  __syncthreads();
+  // logZ = O_E + LSE_c alpha_hat_E[c]  (forward group, warp 0)
+  if (tid < 32) {
+    float x = neg_inf();
+    for (int q = tid; q < C; q += 32) x = fmaxf(x, a.ah[(b * N + Eb) * C + q]);
+    x = warp_max(x);
+    float s = 0.f;
+    if (x != neg_inf())
+      for (int q = tid; q < C; q += 32) s += ex2((a.ah[(b * N + Eb) * C + q] - x) * kLog2e);
+    s = warp_sum(s);
+    if (tid == 0) {
+      const double oE = a.ao[b * N + Eb];
+      const unsigned f = *sflag;
+      float lz;
+      unsigned fl = 0;
+      if (f & TS_F_NONFINITE) {
+        lz = qnan();
+        fl = TS_F_NONFINITE;
+      } else if (x == neg_inf() || !(oE > -INFINITY)) {
+        lz = neg_inf();
+        fl = TS_F_EMPTY;
+      } else {
+        lz = (float)(oE + (double)x + kLn2 * (double)lg2(s));
+        a.zbuf[b] = oE + (double)x + kLn2 * (double)lg2(s);
+      }
+      a.logz[b] = lz;
+      if (a.flags) a.flags[b] = fl;
+      *sflag = fl;
+    }
+  }
+  __syncthreads();
+  if (!mg) return;
+  const unsigned fl = *sflag;
+  const double A = fl ? 0.0 : a.zbuf[b];
+  const float* ah = a.ah + b * N * C;
+  const float* bh = a.bh + b * N * C;
+  const double* ao = a.ao + b * N;
+  const double* bo = a.bo + b * N;
+  for (int64_t q = tid; q < E * KCC; q += blockDim.x) {
+    const int64_t n = q / KCC;
+    const int64_t rem = q - n * KCC;
+    const int k = (int)(rem / ((int64_t)C * C)) + 1;
+    const int c1 = (int)((rem / C) % C), c2 = (int)(rem % C);
+    float v = 0.f;
+    if (!fl && n + k <= Eb) {
+      const double off = ao[n] + bo[n + k] - A;
+      const float x = (float)off + ah[n * C + c1] + pb[q] + bh[(n + k) * C + c2];
+      v = (x == neg_inf() || !(off > -INFINITY)) ? 0.f : ex2(x * kLog2e);
+    }
+    mg[q] = v;
+  }
+}
+
+cudaError_t launch_semimarkov(const SemiArgs& a, cudaStream_t st) {
+  const int R = (int)a.K + 1;
+  const size_t smem = (size_t)2 * R * kSmG * sizeof(float) + (size_t)2 * R * sizeof(double) +
+                      16 * sizeof(float) + 16;
+  semimarkov_kernel<<<(unsigned)a.B, 2 * kSmG, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace tsb
