@@ -97,3 +97,56 @@ def test_product_package_never_imports_oracle():
                 txt = open(os.path.join(dirpath, f)).read()
                 for b in banned:
                     assert b not in txt, (f, b)
+
+
+def test_next_row_entry_points_validate_before_the_device():
+    """The §8(f) / time-sharding entry points reject bad arguments with TS_E_INVALID and,
+    with valid arguments on a machine without an sm_100 device, return TS_E_UNSUPPORTED
+    (there is no CPU fallback) — never a silent success."""
+    L = _lib.load()
+    ch = _chain()
+    A = 0x2000  # an aligned dummy device address (never dereferenced on these paths)
+    # entropy: marg / logz / entropy required
+    assert L.ts_entropy(ctypes.byref(ch), None, A, A, None, None, 0, None) == 1
+    assert L.ts_entropy(ctypes.byref(ch), A, None, A, None, None, 0, None) == 1
+    assert L.ts_entropy(ctypes.byref(ch), A, A, None, None, None, 0, None) == 1
+    # log_prob: z and out required
+    assert L.ts_log_prob(ctypes.byref(ch), None, None, A, None) == 1
+    assert L.ts_log_prob(ctypes.byref(ch), A, None, None, None) == 1
+    # sample: uniforms, K >= 1, z, logz
+    assert L.ts_sample(ctypes.byref(ch), None, 1, A, A, None, None, 0, None) == 1
+    assert L.ts_sample(ctypes.byref(ch), A, 0, A, A, None, None, 0, None) == 1
+    # kbest: 1 <= K <= 16
+    assert L.ts_kbest(ctypes.byref(ch), 0, A, A, None, None, 0, None) == 1
+    assert L.ts_kbest(ctypes.byref(ch), 17, A, A, None, None, 0, None) == 1
+    assert L.ts_kbest_workspace_bytes(ctypes.byref(ch), 17) == 0
+    assert L.ts_kbest_workspace_bytes(ctypes.byref(ch), 4) >= 2 * 4 * 3 * 4 * 2
+    # semimarkov: 1 <= K <= 16, logz required
+    assert L.ts_semimarkov(ctypes.byref(ch), 0, None, A, None, None, 0, None) == 1
+    assert L.ts_semimarkov(ctypes.byref(ch), 2, None, None, None, None, 0, None) == 1
+    # time-sharded Viterbi: lengths must be NULL, rank in [0, world)
+    chl = _chain(lengths=0x3000)
+    assert L.ts_segment_viterbi_summary(ctypes.byref(chl), 0, 5, A, None) == 1
+    assert L.ts_segment_viterbi_maps(ctypes.byref(ch), 0, 5, 2, 2, A, A, None, None, None, 0,
+                                     None) == 1
+    assert L.ts_segment_viterbi_summary_bytes(ctypes.byref(ch)) == 2 * 3 * 3 * 4
+    # valid arguments, no sm_100 device here -> TS_E_UNSUPPORTED
+    import torch
+
+    if not torch.cuda.is_available():
+        assert L.ts_log_prob(ctypes.byref(ch), A, None, A, None) == 2
+        assert L.ts_kbest(ctypes.byref(ch), 4, A, A, None, A, 1 << 20, None) == 2
+        assert L.ts_semimarkov(ctypes.byref(ch), 2, None, A, None, A, 1 << 20, None) == 2
+
+
+def test_next_row_workspace_sizes():
+    L = _lib.load()
+    ch = _chain(B=4, N=100, C=20)
+    assert L.ts_workspace_bytes(ctypes.byref(ch), _lib.TS_OP_ENTROPY, _lib.TS_LOG) >= 4 * 8
+    assert L.ts_workspace_bytes(ctypes.byref(ch), _lib.TS_OP_SAMPLE, _lib.TS_LOG) >= 4 * 100 * 20 * 4
+    assert L.ts_workspace_bytes(ctypes.byref(ch), _lib.TS_OP_SEGMENT_VITERBI,
+                                _lib.TS_MAX) >= 4 * 99 * 20
+    assert L.ts_semimarkov_workspace_bytes(ctypes.byref(ch), 4) >= 2 * 4 * 100 * 20 * 4
+    big = _chain(B=4, N=100, C=200)
+    assert L.ts_workspace_bytes(ctypes.byref(big), _lib.TS_OP_SAMPLE, _lib.TS_LOG) == 0
+    assert L.ts_semimarkov_workspace_bytes(ctypes.byref(big), 4) == 0

@@ -1,7 +1,6 @@
 cd $GRAFT_REPO_ROOT
 O=gpurun_out
-T=tc5
-timeout 60 ./tools/phase_tc8 64 1 > $O/${T}_phase.txt 2>&1
-timeout 60 ./tools/phase_tc8 1024 148 >> $O/${T}_phase.txt 2>&1
-timeout 300 python tools/bench_configs.py --configs 5 --iters 3 > $O/${T}_cfg5.jsonl 2>&1
-timeout 900 python -m pytest tests/test_scan_gpu.py tests/test_segments_gpu.py -x -q --timeout=300 > $O/${T}_tests.log 2>&1; echo "rc=$?" >> $O/${T}_tests.log
+T=san
+for tool in memcheck racecheck synccheck; do
+  timeout 1200 compute-sanitizer --tool $tool --print-limit 20 --error-exitcode 9 python tools/sanitize_all.py > $O/${T}_$tool.log 2>&1; echo "rc=$?" >> $O/${T}_$tool.log
+done
