@@ -125,6 +125,34 @@ def test_cfg4_viterbi_full(dev):
         assert score[b] == np.float32(s)
 
 
+def test_viterbi_full_size_cfg2_cfg3_cfg5(dev):
+    """Bit-exact Viterbi on every BASELINE config (BJ: "bit-exact Viterbi ... on every
+    config"): cfg2 and cfg3 complete, cfg5 (B=4, N=65536, C=128) complete, oracle in
+    generator mode (no 17 GB host buffer)."""
+    import concurrent.futures as cf
+
+    for no in (2, 3, 5):
+        cfg = tsgen.CONFIGS[no]
+        pot = torch.empty((cfg.B, cfg.E, cfg.C, cfg.C), dtype=torch.float32, device=dev)
+        tsgen.fill_torch(pot, cfg)
+        path, score, flags = tsb.viterbi(pot)
+        path, score = path.cpu().numpy(), score.cpu().numpy()
+        del pot
+        torch.cuda.empty_cache()
+        assert (flags.cpu().numpy() == 0).all()
+        bs = range(cfg.B) if no != 3 else (0, 1, 137, 254, 255)
+
+        def one(b, cfg=cfg):
+            return oracle.gen_viterbi(cfg.seed, cfg.quantum, b, cfg.N, cfg.C)
+
+        with cf.ThreadPoolExecutor(8) as ex:
+            res = list(ex.map(one, bs))
+        for b, (p, s, f) in zip(bs, res):
+            assert f == 0
+            np.testing.assert_array_equal(path[b], p)
+            assert score[b] == np.float32(s)
+
+
 def test_cfg3_full_sampled(dev):
     cfg = tsgen.CONFIGS[3]
     pot = torch.empty((cfg.B, cfg.E, cfg.C, cfg.C), dtype=torch.float32, device=dev)
