@@ -171,7 +171,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=0)
     ap.add_argument("--tiny-mode", type=int, default=-1,
-                    help="debug: cfg2 kernel variant (ts_set_tiny: 1 default, 2 overlapped)")
+                    help="debug: cfg2 kernel variant (ts_set_tiny: 1 default, 0 general kernel)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":

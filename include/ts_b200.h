@@ -272,13 +272,11 @@ TS_API int64_t ts_get_plan_chunk(void);
  * distributed shared memory (G in {2, 4}; 0 = the default one-CTA-per-sequence kernel). */
 TS_API void ts_set_small_cluster(int G);
 
-/* Debug/testing knob (process-global): short log-semiring chains with C % 4 == 0 and
- * C <= 28 run through the latency-optimised single-CTA kernel (bulk-copied tiles,
- * lagged-normaliser recursions, mbarrier-published nodes, overlapped marginals): mode 1
- * (default) = prepass then recursions, 2 = prepass overlapped with the recursions (tiles
- * published one by one), 0 = the general single-CTA kernel.  Results agree within the
- * parity tolerances. */
-TS_API void ts_set_tiny(int mode);
+/* Debug/testing knob (process-global): 1 (default) runs short log-semiring chains with
+ * C % 4 == 0 and C <= 28 through the latency-optimised single-CTA kernel (bulk-copied
+ * tiles, lagged-normaliser recursions, mbarrier-published nodes, overlapped marginals);
+ * 0 = the general single-CTA kernel.  Results agree within the parity tolerances. */
+TS_API void ts_set_tiny(int enable);
 
 /* Debug/testing knob (process-global): 1 (default) runs ts_marginals for C = 64 with one
  * serial chunk per sequence as the meet-in-the-middle kernel (forward and backward

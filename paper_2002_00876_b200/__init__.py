@@ -424,11 +424,9 @@ def set_small_cluster(G: int) -> None:
     _lib.load().ts_set_small_cluster(int(G))
 
 
-def set_tiny(mode) -> None:
-    """Debug knob: latency-optimised short-chain kernel for C % 4 == 0, C <= 28:
-    1/True (default) = prepass then recursions, 2 = prepass overlapped with the recursions,
-    0/False = the general kernel."""
-    _lib.load().ts_set_tiny(int(mode))
+def set_tiny(enable: bool) -> None:
+    """Debug knob: latency-optimised short-chain kernel for C % 4 == 0, C <= 28 (default on)."""
+    _lib.load().ts_set_tiny(1 if enable else 0)
 
 
 def set_meet(enable: bool) -> None:

@@ -235,7 +235,7 @@ ts_status run_log(const ts_chain* c, float* marg, float* logz, uint32_t* flags, 
       r = cuda_status(launch_cluster(a, G, st));
       t_kernel = "fb_cluster_kernel";
     } else if (g_tiny.load() && tiny_fits(a)) {
-      r = cuda_status(launch_tiny(a, st, g_tiny.load() == 2));
+      r = cuda_status(launch_tiny(a, st));
       t_kernel = "fb_tiny_kernel";
     } else {
       r = cuda_status(launch_small(a, st));
@@ -1158,7 +1158,7 @@ TS_API int64_t ts_get_plan_chunk(void) { return g_plan_chunk.load(); }
 TS_API void ts_set_small_cluster(int G) {
   g_small_cluster.store((G == 2 || G == 4) ? G : 0);
 }
-TS_API void ts_set_tiny(int mode) { g_tiny.store(mode < 0 ? 0 : (mode > 2 ? 2 : mode)); }
+TS_API void ts_set_tiny(int enable) { g_tiny.store(enable ? 1 : 0); }
 TS_API int ts_last_launch_count(void) { return t_launches; }
 TS_API const char* ts_last_kernel(void) { return t_kernel; }
 

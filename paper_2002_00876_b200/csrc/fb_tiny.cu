@@ -93,7 +93,7 @@ struct TinyLayout {
   int64_t raw, exf, exb, T, F, HF, G, HG, cf, bar, total;  // float offsets
 };
 
-// mbarriers: ld[E] (tile loaded), fn[N], bn[N] (node published), pp[E] (tile prepped)
+// mbarriers: ld[E] (tile loaded), fn[N], bn[N] (node published)
 __host__ __device__ inline TinyLayout tiny_layout(int64_t N, int C) {
   TinyLayout l;
   const int64_t E = N - 1 > 0 ? N - 1 : 1;
@@ -108,7 +108,7 @@ __host__ __device__ inline TinyLayout tiny_layout(int64_t N, int C) {
   l.G = l.HF + N * 32;                 // [N][32] backward linear v_n (slot C: V_n, 31: flag)
   l.HG = l.G + N * 32;                 // [N][32] backward exact log2 v_n
   l.bar = (l.HG + N * 32 + 3) & ~(int64_t)3;
-  l.total = l.bar + 2 * (2 * E + 2 * N) + 8;  // mbarriers (2 floats each) + flag words
+  l.total = l.bar + 2 * (E + 2 * N) + 8;  // mbarriers (2 floats each) + flag words
   return l;
 }
 
@@ -118,10 +118,6 @@ __device__ __forceinline__ float rcp_approx(float x) {
   return y;
 }
 
-// Order in which the two recursions consume tiles: 0, E-1, 1, E-2, ...
-__device__ __forceinline__ int tile_order(int o, int Eb) {
-  return (o & 1) ? Eb - 1 - (o >> 1) : (o >> 1);
-}
 // Order in which edges become ready for marginals (edge t needs forward node t and backward
 // node t+1): centre first, ready(t) = max(t, Eb-1-t).
 __device__ __forceinline__ int edge_order(int q, int Eb) {
@@ -133,11 +129,6 @@ __device__ __forceinline__ int edge_order(int q, int Eb) {
   }
   return (q & 1) ? hi + (q >> 1) : lo - (q >> 1);
 }
-
-// Overlapped prepass: tile t published on the mbarrier pp[t] (a volatile flag + fence.cta
-// measured the same ~500 cycles per recursion step; the mbarrier keeps compute-sanitizer's
-// racecheck able to see the synchronisation).
-__device__ __forceinline__ void tile_wait(uint64_t* pp, int t) { mbar_wait(&pp[t], 0); }
 
 // Exact log2 of node n's vector entry j: recorded by the careful loop (flag slot), else
 // the linear value is >= 2^-60 of its scale and lg2 recovers it.
@@ -165,7 +156,7 @@ template <bool FWD, int C>
 __device__ __forceinline__ int tiny_sweep(const float* __restrict__ Xall, const float* __restrict__ raw,
                                           const float* __restrict__ Tm, float* __restrict__ V,
                                           float* __restrict__ H, float* __restrict__ cinc,
-                                          uint64_t* nb, uint64_t* pp, int Eb, int lane) {
+                                          uint64_t* nb, int Eb, int lane) {
   constexpr int RS = tiny_rs(C), TB = (C + 1) * RS, Q = C / 4;
   const bool act = lane < C;
   const bool live = lane <= C;
@@ -181,7 +172,6 @@ __device__ __forceinline__ int tiny_sweep(const float* __restrict__ Xall, const 
   const float* u = V + n0 * 32;                                          // input node
   uint64_t* np = nb + n0;                                                // input node barrier
   constexpr int dT = FWD ? TB : -TB, dV = FWD ? 32 : -32, dN = FWD ? 1 : -1;
-  if (pp) tile_wait(pp, FWD ? 0 : Eb - 1);  // overlapped prepass: tile published?
   tiny_row<FWD, C>(mp, 0, m);
   int kb = Eb;
   bool prev_bad = false;
@@ -200,10 +190,7 @@ __device__ __forceinline__ int tiny_sweep(const float* __restrict__ Xall, const 
 #endif
     }
     // the next edge's operand (independent of the chain; consumed next step)
-    if (k + 1 < Eb) {
-      if (pp) tile_wait(pp, FWD ? k + 1 : Eb - 2 - k);
-      tiny_row<FWD, C>(mp + dT, 0, mn);
-    }
+    if (k + 1 < Eb) tiny_row<FWD, C>(mp + dT, 0, mn);
     const float r = rcp_approx(U);
     float sa[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
@@ -248,7 +235,6 @@ __device__ __forceinline__ int tiny_sweep(const float* __restrict__ Xall, const 
     const int nin = FWD ? t : t + 1;
     const int nout = FWD ? t + 1 : t;
     float w[C];
-    if (pp) tile_wait(pp, t);
     tiny_row<FWD, C>(Xall + (int64_t)t * TB, row, w);
     const float* u = V + nin * 32;
     const float U = u[C];
@@ -305,10 +291,7 @@ __device__ __forceinline__ int tiny_sweep(const float* __restrict__ Xall, const 
 
 }  // namespace
 
-// OVL: the prepass runs on the 14 marginal warps in the order the recursions consume tiles
-// (0, E-1, 1, E-2, ...), publishing each tile on pp[t]; the recursions start as soon as
-// their first tile is published instead of after the whole prepass.
-template <int C, bool OVL>
+template <int C>
 __global__ void __launch_bounds__(kTinyThreads, 1) fb_tiny_kernel(SmallArgs a) {
   extern __shared__ __align__(16) float sm[];
   constexpr int RS = tiny_rs(C), TB = (C + 1) * RS, CC = C * C, Q4 = CC / 4, Q = C / 4;
@@ -329,14 +312,11 @@ __global__ void __launch_bounds__(kTinyThreads, 1) fb_tiny_kernel(SmallArgs a) {
   uint64_t* ld = reinterpret_cast<uint64_t*>(sm + Lay.bar);
   uint64_t* fn = ld + Ea;
   uint64_t* bn = fn + N;
-  uint64_t* pp = bn + N;
-  unsigned* sflag = reinterpret_cast<unsigned*>(pp + Ea);
+  unsigned* sflag = reinterpret_cast<unsigned*>(bn + N);
 
   // barriers for every tile / node slot, initialised in parallel before any global access
-  for (int64_t k = tid; k < 2 * E + 2 * N; k += kTinyThreads)
-    mbar_init(k < E ? &ld[k]
-                    : (k < E + N ? &fn[k - E] : (k < E + 2 * N ? &bn[k - E - N] : &pp[k - E - 2 * N])),
-              1);
+  for (int64_t k = tid; k < E + 2 * N; k += kTinyThreads)
+    mbar_init(k < E ? &ld[k] : (k < E + N ? &fn[k - E] : &bn[k - E - N]), 1);
   if (tid == 0) *sflag = 0u;
   fence_mbar_init();
   // programmatic dependent launch: the next kernel in the stream may start its prologue now;
@@ -360,29 +340,16 @@ __global__ void __launch_bounds__(kTinyThreads, 1) fb_tiny_kernel(SmallArgs a) {
   const int Eb = (int)(len - 1);
   const float* src = a.pot + b * E * CC;
   // each warp bulk-copies the tiles it preps
-  const bool worker = !(warp == kFwdWarp || warp == kBwdWarp);
   const int wi = worker_index(warp);
-  if (lane == 0) {
-    if (!OVL) {
-      for (int t = warp; t < Eb; t += kTinyWarps)
-        bulk_load(raw + (int64_t)t * CC, src + (int64_t)t * CC, (uint32_t)(CC * 4), &ld[t]);
-    } else if (worker) {
-      for (int o = wi; o < Eb; o += kWorkers) {
-        const int t = tile_order(o, Eb);
-        bulk_load(raw + (int64_t)t * CC, src + (int64_t)t * CC, (uint32_t)(CC * 4), &ld[t]);
-      }
-    }
-  }
+  if (lane == 0)
+    for (int t = warp; t < Eb; t += kTinyWarps)
+      bulk_load(raw + (int64_t)t * CC, src + (int64_t)t * CC, (uint32_t)(CC * 4), &ld[t]);
   TPHASE(0);
 
-  // ---- prepass: tiles t0 = warp + 32 r and t1 = t0 + 16 (processed together for ILP);
-  // OVL: single tiles in consumption order on the worker warps, each published on pp[t] ----
-  const int it0 = OVL ? (worker ? wi : Eb) : warp;
-  const int itstep = OVL ? kWorkers : 2 * kTinyWarps;
-  for (int item = it0; item < Eb; item += itstep) {
+  // ---- prepass: tiles t0 = warp + 32 r and t1 = t0 + 16 (processed together for ILP) -------
+  for (int t0 = warp; t0 < Eb; t0 += 2 * kTinyWarps) {
     constexpr int NV = (Q4 + 31) / 32;
-    const int t0 = OVL ? tile_order(item, Eb) : item;
-    const int t1 = OVL ? Eb : t0 + kTinyWarps;
+    const int t1 = t0 + kTinyWarps;
     const int nt = t0 < Eb ? (t1 < Eb ? 2 : 1) : 0;
     float4 v[2][NV];
     float mx[2] = {neg_inf(), neg_inf()};
@@ -460,18 +427,14 @@ __global__ void __launch_bounds__(kTinyThreads, 1) fb_tiny_kernel(SmallArgs a) {
           }
         }
       }
-      if (OVL) {
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&pp[t0]);
-      }
     }
   }
-  if (!OVL) __syncthreads();
+  __syncthreads();
   TPHASE(2);
 
   if (warp == kFwdWarp) {
     // ---- forward recursion, then logZ -------------------------------------------------
-    const int kbf = tiny_sweep<true, C>(EXF, raw, Tm, F, HF, cf, fn, OVL ? pp : nullptr, Eb, lane);
+    const int kbf = tiny_sweep<true, C>(EXF, raw, Tm, F, HF, cf, fn, Eb, lane);
     TPHASEW(3);
     // logZ = Σ_t (T_t + ln2 c_t) + ln2 log2 Σ_j u_E[j]  (fp64 offsets, exact log sum);
     // c_t = log2 U_t for fast steps, recorded by the careful loop for t >= kbf
@@ -488,7 +451,7 @@ __global__ void __launch_bounds__(kTinyThreads, 1) fb_tiny_kernel(SmallArgs a) {
     }
   } else if (warp == kBwdWarp) {
     if (mg) {
-      tiny_sweep<false, C>(EXB, raw, Tm, G, HG, nullptr, bn, OVL ? pp : nullptr, Eb, lane);
+      tiny_sweep<false, C>(EXB, raw, Tm, G, HG, nullptr, bn, Eb, lane);
       TPHASEW(4);
     }
   } else {
@@ -510,7 +473,6 @@ __global__ void __launch_bounds__(kTinyThreads, 1) fb_tiny_kernel(SmallArgs a) {
         mbar_wait_sleep(&fn[t], 0, TINY_SLEEP_NS);
         mbar_wait_sleep(&bn[t + 1], 0, TINY_SLEEP_NS);
 #endif
-        if (OVL) tile_wait(pp, t);
 #ifdef TS_PHASE_TIMING
         if (blockIdx.x == 0 && lane == 0 && t < 64) g_tiny_edge[t][0] = clock64();
 #endif
@@ -607,14 +569,14 @@ bool tiny_fits(const SmallArgs& a) {
 }
 
 namespace {
-template <int C, bool OVL>
+template <int C>
 cudaError_t launch_tiny_c(const SmallArgs& a, size_t smem, cudaStream_t st) {
   static std::atomic<uint64_t> attr_mask{0};  // one-time attribute setup per device
   int dev = 0;
   cudaGetDevice(&dev);
   const uint64_t bit = 1ull << (dev & 63);
   if (!(attr_mask.load() & bit)) {
-    cudaError_t e = cudaFuncSetAttribute(fb_tiny_kernel<C, OVL>,
+    cudaError_t e = cudaFuncSetAttribute(fb_tiny_kernel<C>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (e != cudaSuccess) return e;
     attr_mask.fetch_or(bit);
@@ -629,27 +591,22 @@ cudaError_t launch_tiny_c(const SmallArgs& a, size_t smem, cudaStream_t st) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, fb_tiny_kernel<C, OVL>, a);
+  return cudaLaunchKernelEx(&cfg, fb_tiny_kernel<C>, a);
 }
 }  // namespace
 
-template <bool OVL>
-cudaError_t launch_tiny_ovl(const SmallArgs& a, size_t smem, cudaStream_t st) {
+cudaError_t launch_tiny(const SmallArgs& a, cudaStream_t st) {
+  const size_t smem = tiny_smem_bytes(a.N, a.C);
   switch (a.C) {
-    case 4: return launch_tiny_c<4, OVL>(a, smem, st);
-    case 8: return launch_tiny_c<8, OVL>(a, smem, st);
-    case 12: return launch_tiny_c<12, OVL>(a, smem, st);
-    case 16: return launch_tiny_c<16, OVL>(a, smem, st);
-    case 20: return launch_tiny_c<20, OVL>(a, smem, st);
-    case 24: return launch_tiny_c<24, OVL>(a, smem, st);
-    case 28: return launch_tiny_c<28, OVL>(a, smem, st);
+    case 4: return launch_tiny_c<4>(a, smem, st);
+    case 8: return launch_tiny_c<8>(a, smem, st);
+    case 12: return launch_tiny_c<12>(a, smem, st);
+    case 16: return launch_tiny_c<16>(a, smem, st);
+    case 20: return launch_tiny_c<20>(a, smem, st);
+    case 24: return launch_tiny_c<24>(a, smem, st);
+    case 28: return launch_tiny_c<28>(a, smem, st);
     default: return cudaErrorInvalidValue;
   }
-}
-
-cudaError_t launch_tiny(const SmallArgs& a, cudaStream_t st, bool overlap) {
-  const size_t smem = tiny_smem_bytes(a.N, a.C);
-  return overlap ? launch_tiny_ovl<true>(a, smem, st) : launch_tiny_ovl<false>(a, smem, st);
 }
 
 }  // namespace tsb

@@ -27,7 +27,7 @@ cudaError_t launch_small(const SmallArgs& a, cudaStream_t st);
 // latency-optimised variant for C % 4 == 0, C <= 28 (fb_tiny.cu)
 size_t tiny_smem_bytes(int64_t N, int64_t C);
 bool tiny_fits(const SmallArgs& a);
-cudaError_t launch_tiny(const SmallArgs& a, cudaStream_t st, bool overlap);
+cudaError_t launch_tiny(const SmallArgs& a, cudaStream_t st);
 int cluster_g(int64_t B, int64_t N, int sms);
 size_t cluster_smem_bytes(int64_t N, int64_t C, int G);
 bool cluster_fits(int64_t N, int64_t C, int G);

@@ -100,33 +100,6 @@ def test_tiny_matches_general_kernel(dev, tiny_off):
         assert float((m0 - m1).abs().max()) <= 2e-6
 
 
-@pytest.mark.parametrize("C", [4, 20, 28])
-def test_tiny_overlapped_prepass_mode(dev, C):
-    """Mode 2 (prepass overlapped with the recursions): same parity gates, every case."""
-    tsb.set_tiny(2)
-    try:
-        for N in (1, 2, 17, 25, 40):
-            parity(tsgen.potentials(3, N, C, seed=900 + N + C), None, dev)
-        B, N = 9, 30
-        pot = tsgen.potentials(B, N, C, seed=C + 3)
-        lengths = tsgen.random_lengths(B, N, C)
-        lengths[0], lengths[1] = 1, N
-        pot[2] = -np.inf
-        pot[3, 4, 1, 2] = np.nan
-        lengths[5] = 0
-        lengths[2] = lengths[3] = N
-        parity(pot, lengths, dev)
-        parity(tsgen.peaked_potentials(3, 25, C, seed=C), None, dev)
-        pot = tsgen.potentials(4, 25, C, seed=77, s=10)
-        for b in range(4):
-            t, j = 5 + 3 * b, (b + 1) % C
-            pot[b, t, :, j] = -200.0
-            pot[b, t + 1, j, :] = 200.0 + pot[b, t + 1, j, :]
-        parity(pot.astype(np.float32), None, dev)
-    finally:
-        tsb.set_tiny(1)
-
-
 def test_tiny_cfg2_sum_to_one_and_deterministic(dev):
     cfg = tsgen.CONFIGS[2]
     pot = torch.from_numpy(tsgen.config_potentials(cfg)).to(dev)

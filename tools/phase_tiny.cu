@@ -5,9 +5,6 @@
 #include <cstdlib>
 #include <vector>
 #include "../paper_2002_00876_b200/csrc/fb_tiny.cu"
-#ifndef OVLMODE
-#define OVLMODE false
-#endif
 using namespace tsb;
 int main(int argc, char** argv) {
   const int B = argc > 1 ? atoi(argv[1]) : 32, N = argc > 2 ? atoi(argv[2]) : 25,
@@ -19,7 +16,7 @@ int main(int argc, char** argv) {
   cudaMalloc(&pot, n * 4); cudaMalloc(&marg, n * 4); cudaMalloc(&logz, B * 4); cudaMalloc(&flags, B * 4);
   cudaMemcpy(pot, h.data(), n * 4, cudaMemcpyHostToDevice);
   SmallArgs a{pot, nullptr, B, N, C, marg, logz, flags};
-  for (int it = 0; it < 5; ++it) launch_tiny(a, 0, OVLMODE);
+  for (int it = 0; it < 5; ++it) launch_tiny(a, 0);
   cudaDeviceSynchronize();
   static long long ph[1024][8];
   cudaMemcpyFromSymbol(ph, g_tiny_phase, sizeof(ph));
@@ -48,7 +45,7 @@ int main(int argc, char** argv) {
   printf("\n");
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
   cudaEventRecord(e0);
-  for (int it = 0; it < 200; ++it) launch_tiny(a, 0, OVLMODE);
+  for (int it = 0; it < 200; ++it) launch_tiny(a, 0);
   cudaEventRecord(e1); cudaEventSynchronize(e1);
   float ms; cudaEventElapsedTime(&ms, e0, e1);
   printf("avg per launch (back-to-back eager, warm L2): %.2f us  err=%s\n", ms * 5.f,
