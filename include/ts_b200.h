@@ -121,7 +121,7 @@ TS_API ts_status ts_viterbi(const ts_chain *c, int32_t *path, float *score, uint
  * at node n; a labelled segmentation of nodes 0 .. len-1 scores the sum of its segments.
  * K = 1 is exactly the linear chain.  Segmental forward-backward (per-cell max, fp64
  * offsets): logz [B] out (required); marg (same layout as pot, 0 for parts that end beyond
- * the sequence) out or NULL; flags as ts_marginals.  C <= 128.
+ * the sequence) out or NULL; flags as ts_marginals.  C <= 256.
  * ws: ts_semimarkov_workspace_bytes(c, K) bytes, 256-byte aligned. */
 TS_API size_t ts_semimarkov_workspace_bytes(const ts_chain *c, int64_t K);
 TS_API ts_status ts_semimarkov(const ts_chain *c, int64_t K, float *marg, float *logz,

@@ -202,6 +202,27 @@ size_t vit_ws(const ts_chain* c, bool need_path, bool need_score, void* ws, VitW
   return cv.off;
 }
 
+// workspace of the exact SIMT segmental kernel (semimarkov.cu), also the K = 1 fallback of
+// the log semiring for long chains with 128 < C <= 256
+size_t semi_ws(const ts_chain* c, int64_t K, void* ws, SemiArgs* a) {
+  Carve cv(ws);
+  const int64_t B = c->B, N = c->N, C = c->C;
+  float* ah = cv.take<float>((size_t)(B * N * C));
+  float* bh = cv.take<float>((size_t)(B * N * C));
+  double* ao = cv.take<double>((size_t)(B * N));
+  double* bo = cv.take<double>((size_t)(B * N));
+  double* zb = cv.take<double>((size_t)B);
+  if (a) {
+    a->ah = ah;
+    a->bh = bh;
+    a->ao = ao;
+    a->bo = bo;
+    a->zbuf = zb;
+    a->K = K;
+  }
+  return cv.off;
+}
+
 size_t op_ws(const ts_chain* c, int op, ts_semiring s, void* ws, StreamWs* sw, VitWs* vw) {
   if (s == TS_MAX) {
     switch (op) {
@@ -213,6 +234,7 @@ size_t op_ws(const ts_chain* c, int op, ts_semiring s, void* ws, StreamWs* sw, V
   }
   if (op == TS_OP_VITERBI) return vit_ws(c, false, false, ws, vw);
   const Plan p = log_plan(c);
+  if (p.kind == PlanKind::Unsupported) return c->C <= 256 ? semi_ws(c, 1, ws, nullptr) : 0;
   if (p.kind != PlanKind::Stream) return 0;
   return stream_ws(c, p, op == TS_OP_MARG, ws, sw, nullptr);
 }
@@ -226,7 +248,28 @@ ts_status cuda_status(cudaError_t e) {
 ts_status run_log(const ts_chain* c, float* marg, float* logz, uint32_t* flags, void* ws,
                   size_t ws_bytes, cudaStream_t st) {
   const Plan p = log_plan(c);
-  if (p.kind == PlanKind::Unsupported) return TS_E_UNSUPPORTED;
+  if (p.kind == PlanKind::Unsupported) {
+    if (c->C > 256) return TS_E_UNSUPPORTED;
+    // long chains with 128 < C <= 256: the exact SIMT segmental kernel with K = 1 (= the
+    // linear chain, reading R17), forward and backward recursions concurrently
+    SemiArgs sa{};
+    const size_t need = semi_ws(c, 1, ws, &sa);
+    if (ws_bytes < need || !ws || !aligned(ws, kAlign)) return TS_E_WORKSPACE;
+    sa.pot = c->pot;
+    sa.lengths = c->lengths;
+    sa.B = c->B;
+    sa.N = c->N;
+    sa.C = c->C;
+    sa.marg = marg;
+    sa.logz = logz;
+    sa.flags = flags;
+    ts_status r = cuda_status(launch_semimarkov(sa, st));
+    if (r == TS_OK) {
+      t_launches = 1;
+      t_kernel = "semimarkov_kernel";
+    }
+    return r;
+  }
   if (p.kind == PlanKind::Small) {
     SmallArgs a{c->pot, c->lengths, c->B, c->N, c->C, marg, logz, flags};
     const int G = g_small_cluster.load();
@@ -602,15 +645,8 @@ TS_API size_t ts_workspace_bytes(const ts_chain* c, int op, ts_semiring s) {
 }
 
 TS_API size_t ts_semimarkov_workspace_bytes(const ts_chain* c, int64_t K) {
-  if (!chain_ok(c) || K < 1 || K > 16 || c->C > 128) return 0;
-  Carve cv(nullptr);
-  const int64_t B = c->B, N = c->N, C = c->C;
-  cv.take<float>((size_t)(B * N * C));
-  cv.take<float>((size_t)(B * N * C));
-  cv.take<double>((size_t)(B * N));
-  cv.take<double>((size_t)(B * N));
-  cv.take<double>((size_t)B);
-  return cv.off;
+  if (!chain_ok(c) || K < 1 || K > 16) return 0;
+  return semi_ws(c, K, nullptr, nullptr);
 }
 
 TS_API ts_status ts_semimarkov(const ts_chain* c, int64_t K, float* marg, float* logz,
@@ -618,27 +654,18 @@ TS_API ts_status ts_semimarkov(const ts_chain* c, int64_t K, float* marg, float*
   if (!chain_ok(c) || K < 1 || K > 16 || !logz || !aligned(logz, 4) ||
       (marg && !aligned(marg, 4)) || (flags && !aligned(flags, 4)))
     return TS_E_INVALID;
-  if (c->C > 128) return TS_E_UNSUPPORTED;
   if (!device_ok()) return TS_E_UNSUPPORTED;
-  const size_t need = ts_semimarkov_workspace_bytes(c, K);
-  if (ws_bytes < need || !ws || !aligned(ws, kAlign)) return TS_E_WORKSPACE;
-  Carve cv(ws);
-  const int64_t B = c->B, N = c->N, C = c->C;
   SemiArgs a{};
+  const size_t need = semi_ws(c, K, ws, &a);
+  if (ws_bytes < need || !ws || !aligned(ws, kAlign)) return TS_E_WORKSPACE;
   a.pot = c->pot;
   a.lengths = c->lengths;
-  a.B = B;
-  a.N = N;
-  a.C = C;
-  a.K = K;
+  a.B = c->B;
+  a.N = c->N;
+  a.C = c->C;
   a.marg = marg;
   a.logz = logz;
   a.flags = flags;
-  a.ah = cv.take<float>((size_t)(B * N * C));
-  a.bh = cv.take<float>((size_t)(B * N * C));
-  a.ao = cv.take<double>((size_t)(B * N));
-  a.bo = cv.take<double>((size_t)(B * N));
-  a.zbuf = cv.take<double>((size_t)B);
   ts_status r = cuda_status(launch_semimarkov(a, static_cast<cudaStream_t>(stream)));
   if (r == TS_OK) {
     t_launches = 1;

@@ -3,34 +3,37 @@
 // reading R17: pot [B][N-1][K][C][C], l[b,n,k-1,c1,c2] scores a segment covering the k
 // steps n -> n+k with label c2 after label c1 at node n; K = 1 is the linear chain).
 //
-// Segmental forward-backward, one CTA per sequence: threads 0..127 run the forward
-// recursion (thread c), threads 128..255 the backward recursion concurrently:
+// Segmental forward-backward, one CTA per sequence: the first GS threads (GS = 128 or 256
+// >= C) run the forward recursion (thread c), the next GS the backward one concurrently:
 //   alpha_p[c] = LSE_{k <= min(K,p), c'} alpha_{p-k}[c'] + l[p-k, k-1, c', c]
 //   beta_p[c]  = LSE_{k <= min(K,E-p), c'} l[p, k-1, c, c'] + beta_{p+k}[c']
 // with the per-cell max of §6(c) and node vectors stored normalised (max 0) with
 // fp64 natural offsets (the last K+1 vectors also in an SMEM ring).  Then all threads write
 //   mu[n,k-1,c1,c2] = exp(alpha_n[c1] + l[n,k-1,c1,c2] + beta_{n+k}[c2] - A)
-// (0 for parts beyond the sequence).  Flags as the linear chain.
+// (0 for parts beyond the sequence).  Flags as the linear chain.  With K = 1 this is also
+// the exact fallback of ts_logpartition / ts_marginals for long chains with 128 < C <= 256.
 #include "common.cuh"
 #include "kernels.cuh"
 
 namespace tsb {
 
 namespace {
-constexpr int kSmG = 128;  // threads per recursion group (C <= 128)
-
+template <int GS>
 __device__ __forceinline__ float group_max(float v, float* red, int gw, int bar_id) {
   v = warp_max(v);
   if ((threadIdx.x & 31) == 0) red[gw] = v;
-  named_bar(bar_id, kSmG);
+  named_bar(bar_id, GS);
   float r = red[0];
-  for (int k = 1; k < kSmG / 32; ++k) r = fmaxf(r, red[k]);
-  named_bar(bar_id, kSmG);
+  for (int k = 1; k < GS / 32; ++k) r = fmaxf(r, red[k]);
+  named_bar(bar_id, GS);
   return r;
 }
 }  // namespace
 
-__global__ void __launch_bounds__(2 * kSmG) semimarkov_kernel(SemiArgs a) {
+// GS = threads per recursion group: 128 (C <= 128) or 256 (C <= 256)
+template <int GS>
+__global__ void __launch_bounds__(2 * GS) semimarkov_kernel(SemiArgs a) {
+  constexpr int kSmG = GS;
   extern __shared__ __align__(16) float ssm[];
   const int C = (int)a.C, K = (int)a.K;
   const int64_t N = a.N, E = N - 1, KCC = (int64_t)K * C * C;
@@ -105,7 +108,7 @@ __global__ void __launch_bounds__(2 * kSmG) semimarkov_kernel(SemiArgs a) {
         }
       }
     const float val = (act && m != neg_inf()) ? m + lg2(sum) * (float)kLn2 : neg_inf();
-    const float M = group_max(val, red, gw, 1 + grp);
+    const float M = group_max<GS>(val, red, gw, 1 + grp);
     const bool dead = (M == neg_inf());
     const float nv = (act && !dead) ? val - M : neg_inf();
     ring[(p % R) * kSmG + c] = nv;
@@ -173,9 +176,13 @@ __global__ void __launch_bounds__(2 * kSmG) semimarkov_kernel(SemiArgs a) {
 
 cudaError_t launch_semimarkov(const SemiArgs& a, cudaStream_t st) {
   const int R = (int)a.K + 1;
-  const size_t smem = (size_t)2 * R * kSmG * sizeof(float) + (size_t)2 * R * sizeof(double) +
+  const int GS = a.C <= 128 ? 128 : 256;
+  const size_t smem = (size_t)2 * R * GS * sizeof(float) + (size_t)2 * R * sizeof(double) +
                       16 * sizeof(float) + 16;
-  semimarkov_kernel<<<(unsigned)a.B, 2 * kSmG, smem, st>>>(a);
+  if (GS == 128)
+    semimarkov_kernel<128><<<(unsigned)a.B, 256, smem, st>>>(a);
+  else
+    semimarkov_kernel<256><<<(unsigned)a.B, 512, smem, st>>>(a);
   return cudaGetLastError();
 }
 

@@ -97,6 +97,18 @@ def test_cfg3_reduced_elementwise(dev):
     assert_viterbi_parity(pot, None, dev)
 
 
+@pytest.mark.parametrize("B,N,C", [(2, 70, 130), (3, 40, 200), (2, 30, 256), (2, 2, 256)])
+def test_log_semiring_wide_labels(dev, B, N, C):
+    """128 < C <= 256 on chains that do not fit one CTA: the exact SIMT segmental kernel with
+    K = 1 (reading R17 reduces to the linear chain)."""
+    pot = tsgen.potentials(B, N, C, seed=900 + N + C)
+    assert_log_parity(pot, None, dev)
+    lengths = np.array([N] + [max(1, N // 3)] * (B - 1), np.int32)
+    assert_log_parity(pot, lengths, dev)
+    pot[0, N // 2 - 1, 3, 4] = np.nan
+    assert_log_parity(pot, None, dev)
+
+
 @pytest.mark.parametrize("C", [3, 20, 64, 130, 256])
 def test_viterbi_shapes(dev, C):
     pot = tsgen.potentials(3, 70, C, seed=77 + C)

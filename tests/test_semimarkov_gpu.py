@@ -30,7 +30,7 @@ def _parity(pot, dev, lengths=None):
 
 @pytest.mark.parametrize("B,N,K,C", [(2, 6, 3, 4), (3, 25, 4, 20), (2, 40, 8, 16),
                                      (2, 20, 16, 8), (2, 12, 3, 100), (2, 2, 4, 5),
-                                     (1, 1, 2, 3), (2, 33, 5, 128)])
+                                     (1, 1, 2, 3), (2, 33, 5, 128), (2, 9, 3, 200)])
 def test_semimarkov_parity(dev, B, N, K, C):
     err = _parity(_pot(B, N, K, C, N * K + C), dev)
     assert err < 1e-5
