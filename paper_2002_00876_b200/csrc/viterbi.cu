@@ -92,14 +92,36 @@ __global__ void __launch_bounds__(256) viterbi_fwd_kernel(VitArgs a, int S, int 
     const float* tile = ring + (size_t)(g % S) * SF;
     const float* d = dl + buf * NT + r0;
     if (act) {
-#pragma unroll 4
-      for (int r = 0; r < nr; ++r) {
-        const float v = d[r] + tile[r * C + tid];
-        chk = max_nan(chk, v);
-        if (v > best) {
-          best = v;
+      // two interleaved row streams (independent compare chains), merged with the
+      // smallest-index rule on ties (reading R5)
+      float best1 = neg_inf();
+      int arg1 = 0x7fffffff;
+      int r = 0;
+#pragma unroll 2
+      for (; r + 1 < nr; r += 2) {
+        const float v0 = d[r] + tile[r * C + tid];
+        const float v1 = d[r + 1] + tile[(r + 1) * C + tid];
+        chk = max_nan(chk, max_nan(v0, v1));
+        if (v0 > best) {
+          best = v0;
           arg = r0 + r;
         }
+        if (v1 > best1) {
+          best1 = v1;
+          arg1 = r0 + r + 1;
+        }
+      }
+      if (r < nr) {
+        const float v0 = d[r] + tile[r * C + tid];
+        chk = max_nan(chk, v0);
+        if (v0 > best) {
+          best = v0;
+          arg = r0 + r;
+        }
+      }
+      if (best1 > best || (best1 == best && arg1 < arg)) {
+        best = best1;
+        arg = arg1;
       }
     }
     if (blk == nblk - 1) {
@@ -301,7 +323,12 @@ cudaError_t launch_vit1(const VitArgs& a, cudaStream_t st) {
   const int C = (int)a.C;
   const int RB = vit_rows(C);
   const size_t stage = (((size_t)RB * C) + 3) & ~(size_t)3;
-  int S = (int)((160 * 1024) / (stage * 4));
+  // stages sized for occupancy: ceil(B / #SMs) CTAs should be resident per SM (up to 4)
+  int sms = 148, dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int64_t per_sm = (a.B + sms - 1) / sms;
+  per_sm = per_sm < 1 ? 1 : (per_sm > 4 ? 4 : per_sm);
+  int S = (int)(((200 * 1024) / per_sm) / (stage * 4));
   S = S < 2 ? 2 : (S > 8 ? 8 : S);
   const bool vec4 = (C % 4) == 0 && (reinterpret_cast<uintptr_t>(a.pot) & 15) == 0;
   const size_t smem = vit_smem_bytes(C, S, RB);
