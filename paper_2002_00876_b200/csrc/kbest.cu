@@ -59,8 +59,15 @@ __global__ void __launch_bounds__(256) kbest_kernel(KbestArgs a) {
     const float* d = dl + (size_t)cur * C * KM;
     if (act) {
       const float* col = a.pot + (b * E + t) * CC + tid;
-      for (int i = 0; i < C; ++i) {
-        const float lv = col[(int64_t)i * C];
+      constexpr int kPf = 16;  // column values loaded per batch (independent loads in flight)
+      for (int i0 = 0; i0 < C; i0 += kPf) {
+        float lvs[kPf];
+#pragma unroll
+        for (int u = 0; u < kPf; ++u) lvs[u] = (i0 + u < C) ? col[(int64_t)(i0 + u) * C] : neg_inf();
+#pragma unroll 1
+        for (int u = 0; u < kPf && i0 + u < C; ++u) {
+        const int i = i0 + u;
+        const float lv = lvs[u];
         nonfin |= (lv != lv) | (lv == pos_inf());
         if (lv == neg_inf()) continue;
         for (int r = 0; r < KM; ++r) {
@@ -83,6 +90,7 @@ __global__ void __launch_bounds__(256) kbest_kernel(KbestArgs a) {
               ii[p] = i;
               rr[p] = r;
             }
+        }
         }
       }
       float* dn = dl + (size_t)(cur ^ 1) * C * KM + (size_t)tid * KM;
