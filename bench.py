@@ -159,6 +159,86 @@ def run_reference(args):
     return 0
 
 
+def run_time_sharded(args):
+    """Side mode (not the driver's line): cfg5-style long chains split in TIME across the
+    ranks: each rank generates its edge range in place, runs the local scan
+    summary, one NCCL all_gather_into_tensor of the C x C summaries, then the combine and its
+    local sweeps + marginals.  Total work is fixed as N grows ("scaling": "strong").  Time =
+    max over ranks of CUDA-event time around K steps (summary + all-gather + finish)."""
+    import torch
+
+    import paper_2002_00876_b200 as tsb
+    import tsgen
+    from paper_2002_00876_b200 import dist as tdist
+
+    rank, local_rank, world = env_rank()
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = tsgen.CONFIGS[args.config]
+    B, N, C, E = cfg.B, cfg.N, cfg.C, cfg.E
+    begin, count = tdist.shard_edges(E, world, rank)
+    local = torch.empty((B, count, C, C), dtype=torch.float32, device=dev)
+    tsgen.fill_torch(local, cfg.seed, cfg.quantum, t_begin=begin, E_global=E)
+    seg = tsb.Segment(local, begin, N)
+    marg = None
+
+    def step():
+        nonlocal marg
+        summ = seg.summary()
+        gathered = tdist._all_gather(summ, None) if dist is not None else summ[None]
+        marg, logz, flags = seg.finish(gathered, rank, world, True)
+        return logz, flags
+
+    for _ in range(args.warmup):
+        logz, flags = step()
+    torch.cuda.synchronize(dev)
+    assert int(flags.abs().sum()) == 0
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    ev0.record()
+    for _ in range(args.steps):
+        step()
+    ev1.record()
+    torch.cuda.synchronize(dev)
+    sampler.stop()
+    ms_t = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device=dev)
+    if dist is not None:
+        dist.barrier()
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t.item()) / args.steps
+    if rank == 0:
+        peak, peak_src = load_peaks()
+        alg = 8 * B * E * C * C
+        line = {"metric": f"tokens/sec linear-chain logZ+marginals time-sharded (cfg{cfg.no}: "
+                          f"B={B},N={N},C={C})", "value": B * N / (ms / 1e3), "unit": UNIT,
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                "dtype": "f32", "data": "synthetic (tsgen, generated in place per rank)",
+                "config": {"workload": f"cfg{cfg.no}: {cfg.label}",
+                           "parallelism": f"time-sharded over {world} GPU(s), one NCCL "
+                                          "all_gather of C x C segment summaries per step",
+                           "l2": f"inputs {alg / 2 / 1e9:.1f} GB >> L2"},
+                "roofline": {"bound": "hbm", "achieved": alg / (ms / 1e3) / 1e9 / world,
+                             "peak": peak, "unit": "GB/s (per GPU)",
+                             "frac": alg / (ms / 1e3) / 1e9 / world / peak,
+                             "peak_source": peak_src},
+                "clocks": sampler.summary()}
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -170,12 +250,16 @@ def main():
     ap.add_argument("--sets", type=int, default=0, help="rotating buffer sets (0 = auto > 2x L2)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=0)
+    ap.add_argument("--time-shard", action="store_true",
+                    help="side mode: time-sharded long chains (use with --config 5)")
     ap.add_argument("--tiny-mode", type=int, default=-1,
                     help="debug: cfg2 kernel variant (ts_set_tiny: 1 default, 0 general kernel)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         return run_reference(args)
+    if args.time_shard:
+        return run_time_sharded(args)
 
     import torch
 
