@@ -299,36 +299,55 @@ __global__ void __launch_bounds__(kScanThreads) tree_up_kernel(ScanArgs a, int l
   constexpr int CP = 128;
   float* wT = sm;            // [CP][CP] wT[i][r] = 2^W[r][i]
   float* e2 = wT + CP * CP;  // [CP][CP] e2[i][j] = 2^S2[i][j]
-  float* R = e2 + CP * CP;   // [C][C] log2 results
-  double* ref = reinterpret_cast<double*>(R + CP * CP);  // [C]
+  float* R = e2 + CP * CP;   // [C][C] log2 results; first the staged S1 rows (stride CP+1)
+  double* ref = reinterpret_cast<double*>(R + CP * (CP + 1));  // [CP] row maxima
+  double* O2s = ref + CP;                                      // [CP] staged O2
   const float* S1g = a.mat + n1 * CC;
   const double* O1 = a.off + n1 * C;
   const float* S2g = a.mat + n2 * CC;
   const double* O2 = a.off + n2 * C;
+  // stage S1 (coalesced global reads; padded stride -> conflict-free column reads) and O2
+  for (int q = tid; q < CC; q += kScanThreads) {
+    const int r = q / C, i = q - (q / C) * C;
+    R[r * (CP + 1) + i] = S1g[q];
+  }
+  for (int i = tid; i < C; i += kScanThreads) O2s[i] = O2[i];
   for (int q = tid; q < CP * CP; q += kScanThreads) {
     const int i = q >> 7, j = q & (CP - 1);
     e2[q] = (i < C && j < C) ? ex2(S2g[i * C + j]) : 0.f;
   }
-  for (int r = tid; r < CP; r += kScanThreads) {
-    if (r >= C) {
-      for (int i = 0; i < CP; ++i) wT[i * CP + r] = 0.f;
-      continue;
-    }
-    double m = -INFINITY;
-    for (int i = 0; i < C; ++i) {
-      const float s1 = S1g[r * C + i];
-      if (s1 != neg_inf()) {
-        const double c = kLn2 * (double)s1 + O2[i];
-        m = c > m ? c : m;
+  __syncthreads();
+  {  // row maxima ref_r = max_i (ln2 S1[r][i] + O2[i]): one warp per row, lanes over i
+    const int lane = tid & 31, w = tid >> 5;
+    for (int r = w; r < C; r += kScanThreads / 32) {
+      double m = -INFINITY;
+      for (int i = lane; i < C; i += 32) {
+        const float s1 = R[r * (CP + 1) + i];
+        if (s1 != neg_inf()) {
+          const double c = kLn2 * (double)s1 + O2s[i];
+          m = c > m ? c : m;
+        }
       }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double x = __shfl_xor_sync(0xffffffffu, m, o);
+        m = x > m ? x : m;
+      }
+      if (lane == 0) ref[r] = m;
     }
-    ref[r] = m;
-    for (int i = 0; i < CP; ++i) {
-      const float s1 = i < C ? S1g[r * C + i] : neg_inf();
-      wT[i * CP + r] = (s1 == neg_inf() || m == -INFINITY)
-                           ? 0.f
-                           : ex2((float)((kLn2 * (double)s1 + O2[i] - m) * (double)kLog2e));
+  }
+  __syncthreads();
+  // wT[i][r] = 2^((ln2 S1[r][i] + O2[i] - ref_r) log2 e), flat over (i, r): coalesced stores
+  for (int q = tid; q < CP * CP; q += kScanThreads) {
+    const int i = q >> 7, r = q & (CP - 1);
+    float v = 0.f;
+    if (i < C && r < C) {
+      const float s1 = R[r * (CP + 1) + i];
+      const double m = ref[r];
+      if (s1 != neg_inf() && m != -INFINITY)
+        v = ex2((float)((kLn2 * (double)s1 + O2s[i] - m) * (double)kLog2e));
     }
+    wT[q] = v;
   }
   __syncthreads();
   {
@@ -389,12 +408,17 @@ __global__ void __launch_bounds__(kScanThreads) tree_up_kernel(ScanArgs a, int l
     }
   }
   __syncthreads();
-  for (int r = tid; r < C; r += kScanThreads) {
-    float m = neg_inf();
-    for (int j = 0; j < C; ++j) m = fmaxf(m, R[r * C + j]);
-    const bool dead = (m == neg_inf()) || ref[r] == -INFINITY;
-    for (int j = 0; j < C; ++j) Sd[r * C + j] = dead ? neg_inf() : R[r * C + j] - m;
-    Od[r] = dead ? 0.0 : O1[r] + ref[r] + kLn2 * (double)m;
+  // row normalisation: one warp per row, lanes over j (conflict-free SMEM, coalesced stores)
+  {
+    const int lane = tid & 31, w = tid >> 5;
+    for (int r = w; r < C; r += kScanThreads / 32) {
+      float m = neg_inf();
+      for (int j = lane; j < C; j += 32) m = fmaxf(m, R[r * C + j]);
+      m = warp_max(m);
+      const bool dead = (m == neg_inf()) || ref[r] == -INFINITY;
+      for (int j = lane; j < C; j += 32) Sd[r * C + j] = dead ? neg_inf() : R[r * C + j] - m;
+      if (lane == 0) Od[r] = dead ? 0.0 : O1[r] + ref[r] + kLn2 * (double)m;
+    }
   }
   if (tid == 0) a.ident[nd] = 0;
 }
@@ -453,13 +477,18 @@ __device__ void mat_vec(const float* S, const double* So, const float* v, double
                         float* out, double* out_off, float* scratch, int tid) {
   double* tot = reinterpret_cast<double*>(scratch);  // [C]
   double* dref = tot + C;
-  for (int r = tid; r < C; r += kScanThreads) {
-    float m = neg_inf();
-    for (int j = 0; j < C; ++j) m = fmaxf(m, S[r * C + j] + v[j]);
-    float s = 0.f;
-    if (m != neg_inf())
-      for (int j = 0; j < C; ++j) s += ex2(S[r * C + j] + v[j] - m);
-    tot[r] = (m == neg_inf()) ? -INFINITY : So[r] + vo + kLn2 * (double)(m + lg2(s));
+  {  // one warp per row, lanes over j (conflict-free SMEM row reads)
+    const int lane = tid & 31, w = tid >> 5;
+    for (int r = w; r < C; r += kScanThreads / 32) {
+      float m = neg_inf();
+      for (int j = lane; j < C; j += 32) m = fmaxf(m, S[r * C + j] + v[j]);
+      m = warp_max(m);
+      float s = 0.f;
+      if (m != neg_inf())
+        for (int j = lane; j < C; j += 32) s += ex2(S[r * C + j] + v[j] - m);
+      s = warp_sum(s);
+      if (lane == 0) tot[r] = (m == neg_inf()) ? -INFINITY : So[r] + vo + kLn2 * (double)(m + lg2(s));
+    }
   }
   __syncthreads();
   if (tid == 0) {
@@ -760,9 +789,9 @@ cudaError_t launch_fast(const ScanArgs& a, cudaStream_t st) {
 }
 }  // namespace
 
-size_t scan_mat_smem(int64_t C) {  // tree_up: 3 [128][128] fp32 buffers + fp64 row refs
+size_t scan_mat_smem(int64_t C) {  // tree_up: 2 [128][128] + 1 [128][129] fp32 buffers, 2x128 fp64
   (void)C;
-  return (size_t)(3 * 128 * 128) * 4 + (size_t)128 * 8 + 64;
+  return (size_t)(2 * 128 * 128 + 128 * 129) * 4 + (size_t)2 * 128 * 8 + 64;
 }
 
 cudaError_t launch_scan_up(const ScanArgs& a, cudaStream_t st, int* launches) {
