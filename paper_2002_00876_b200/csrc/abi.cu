@@ -458,11 +458,16 @@ bool seg_ok(const ts_chain* c, int64_t edge_begin, int64_t n_global) {
 
 // ts_marginals_host pipelining: the batch is cut into K chunks, each on its own library
 // stream (H2D -> kernels -> D2H), so chunk k's copy back overlaps chunk k+1's kernels and
-// copy in (the two copy directions run on separate engines).  Chunks of >= 256 KB.
-constexpr int kHostMaxChunks = 4;
+// copy in (the two copy directions run on separate engines).  Chunks of >= 4 MB.
+#ifndef TS_HOST_MAX_CHUNKS
+#define TS_HOST_MAX_CHUNKS 4
+#endif
+constexpr int kHostMaxChunks = TS_HOST_MAX_CHUNKS;
 int host_chunks(int64_t B, int64_t per_seq_floats) {
+  // >= 4 MB per chunk: splitting a 1.2 MB transfer into 4 streams measured slower on the
+  // GPU boxes (cfg2 e2e 103 -> 77 us/step with one chunk; tools/e2e_ab.py)
   const int64_t bytes = B * per_seq_floats * 4;
-  int64_t k = bytes / (256 << 10);
+  int64_t k = bytes / (4 << 20);
   if (k > kHostMaxChunks) k = kHostMaxChunks;
   if (k > B) k = B;
   return k < 1 ? 1 : (int)k;

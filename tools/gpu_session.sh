@@ -1,5 +1,5 @@
 cd $GRAFT_REPO_ROOT
 O=gpurun_out
-timeout 60 ./tools/phase_tiny 32 25 20 > $O/g4_phase.txt 2>&1
-timeout 600 python -m pytest tests/test_tiny_gpu.py tests/test_parity_gpu.py -x -q --timeout=600 > $O/g4_tests.log 2>&1; echo "rc=$?" >> $O/g4_tests.log
-for i in 1 2; do timeout 300 python bench.py --no-cpu-baseline --e2e-steps 20 >> $O/g4_bench.jsonl 2>> $O/g4_bench.err; done
+timeout 120 python tools/e2e_ab.py paper_2002_00876_b200/libts_b200.so >> $O/e2eab3.txt 2>&1
+timeout 300 python bench.py --no-cpu-baseline > $O/e2eab3_bench.json 2>/dev/null
+timeout 120 python tools/e2e_ab.py paper_2002_00876_b200/libts_b200.so >> $O/e2eab3.txt 2>&1
