@@ -1,5 +1,7 @@
 cd $GRAFT_REPO_ROOT
 O=gpurun_out
-timeout 120 python tools/e2e_ab.py paper_2002_00876_b200/libts_b200.so >> $O/e2eab3.txt 2>&1
-timeout 300 python bench.py --no-cpu-baseline > $O/e2eab3_bench.json 2>/dev/null
-timeout 120 python tools/e2e_ab.py paper_2002_00876_b200/libts_b200.so >> $O/e2eab3.txt 2>&1
+T=tc6
+timeout 60 ./tools/phase_tc 64 1 > $O/${T}_phase.txt 2>&1
+timeout 60 ./tools/phase_tc 1024 148 >> $O/${T}_phase.txt 2>&1
+timeout 300 python tools/bench_configs.py --configs 5 --iters 3 > $O/${T}_cfg5.jsonl 2>&1
+timeout 900 python -m pytest tests/test_scan_gpu.py tests/test_segments_gpu.py -x -q --timeout=600 > $O/${T}_tests.log 2>&1; echo "rc=$?" >> $O/${T}_tests.log
