@@ -164,3 +164,22 @@ def test_sampling_lengths_flags(dev):
     assert (z[:, 2, 5:] == -1).all() and (z[:, 1, 1:] == -1).all()
     np.testing.assert_array_equal(z[:, 1, 0], ref[:, 1, 0])  # len 1: uniform draw
     assert (fl.cpu().numpy()[[3, 4]] != 0).all()
+
+
+def test_new_ops_deterministic_bitwise(dev):
+    """Identical inputs give bit-identical outputs for every §8(f) entry point."""
+    pot = torch.from_numpy(tsgen.potentials(6, 40, 20, seed=13)).to(dev)
+    u = torch.rand((3, 6, 40), generator=torch.Generator().manual_seed(1)).to(dev)
+    z = torch.randint(0, 20, (6, 40), generator=torch.Generator().manual_seed(2)).to(torch.int32).to(dev)
+    sm = torch.from_numpy(np.random.default_rng(3).standard_normal((3, 19, 4, 12, 12)).astype(
+        np.float32)).to(dev)
+    runs = []
+    for _ in range(2):
+        H, _, _, _ = tsb.entropy(pot)
+        lp = tsb.log_prob(pot, z)
+        zz, _, _ = tsb.sample(pot, u)
+        kp, ks, _ = tsb.kbest(pot, 5)
+        mg, lz, _ = tsb.semimarkov(sm)
+        runs.append([x.clone() for x in (H, lp, zz, kp, ks, mg, lz)])
+    for a, b in zip(*runs):
+        assert torch.equal(a, b)
