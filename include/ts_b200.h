@@ -80,7 +80,8 @@ enum {
   TS_OP_ENTROPY = 5,   /* ts_entropy (TS_LOG)                               */
   TS_OP_SAMPLE = 6,    /* ts_sample (TS_LOG, C <= 128)                      */
   TS_OP_SEGMENT_VITERBI = 7, /* ts_segment_viterbi_maps + _finish (same ws)  */
-  TS_OP_KBEST = 8      /* ts_kbest: size via ts_kbest_workspace_bytes(c, K)  */
+  TS_OP_KBEST = 8,     /* ts_kbest: size via ts_kbest_workspace_bytes(c, K)  */
+  TS_OP_EXPECTATION = 9 /* ts_expectation (TS_LOG; same size as TS_OP_ENTROPY) */
 };
 
 /* One batch of chains.  N >= 1 positions (N-1 edges), 1 <= B, 1 <= C <= 256.
@@ -183,6 +184,19 @@ TS_API ts_status ts_segment_viterbi_finish(const ts_chain *local, int64_t edge_b
  * ws: ts_workspace_bytes(c, TS_OP_ENTROPY, TS_LOG) bytes, 256-byte aligned. */
 TS_API ts_status ts_entropy(const ts_chain *c, float *marg, float *logz, float *entropy,
                             uint32_t *flags, void *ws, size_t ws_bytes, void *stream);
+
+/* Expectation of an additive feature (Table 2 'Exp.' row; the expectation semiring
+ * of li2009first evaluated through the marginals):
+ *     out[b] = E_{z ~ p}[Σ_{t<len-1} r[b][t][z_t][z_{t+1}]] = Σ_{t,i,j} mu[b][t][i][j] r[b][t][i][j]
+ * r [B][N-1][C][C] fp32 device, 16-byte aligned (same layout as pot; required, TS_E_INVALID
+ * when NULL).  Runs the ts_marginals(TS_LOG) hot path into `marg` and `logz` (both required
+ * as for ts_entropy), then the same deterministic two-stage fp64 reduction of mu·r (terms
+ * with mu = 0 skipped, so r may hold anything at masked parts).  out [B] fp32; NaN for
+ * EMPTY / NONFINITE / BADLEN sequences.  r = l gives E_p[Score] = A - H.
+ * ws: ts_workspace_bytes(c, TS_OP_EXPECTATION, TS_LOG) bytes, 256-byte aligned. */
+TS_API ts_status ts_expectation(const ts_chain *c, const float *r, float *marg, float *logz,
+                                float *out, uint32_t *flags, void *ws, size_t ws_bytes,
+                                void *stream);
 
 /* Density: out[b] = Score_b(z) - logz[b] with Score(z) = Σ_{t < len-1}
  * l[b][t][z_t][z_{t+1}] accumulated in fp64.  z [B][N] int32 labels

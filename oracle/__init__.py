@@ -201,6 +201,27 @@ def chain_entropy(pot, lengths=None, threads: int = 1):
     return H, logz, flags
 
 
+def chain_expectation(pot, r, lengths=None, threads: int = 1):
+    """Expectation of an additive feature (Table 2 'Exp.' row): the expectation
+    semiring's moment over all structures divided by their total weight,
+        E_p[Σ_{t<len-1} r_t[z_t][z_{t+1}]] = Σ_t Σ_ij mu_t[i][j] r_t[i][j]
+    by linearity of expectation over the parts.  fp64; terms with mu = 0
+    contribute 0.  NaN for EMPTY / NONFINITE / BADLEN sequences.
+    -> (E [B] f64, logz [B], flags)."""
+    r64 = np.asarray(r, dtype=np.float64)
+    logz, marg, flags = chain_marginals(pot, lengths, want_marg=True, threads=threads)
+    B = r64.shape[0]
+    out = np.empty(B, dtype=np.float64)
+    for b in range(B):
+        if flags[b] != 0:
+            out[b] = math.nan
+            continue
+        m = marg[b]
+        nz = m != 0.0
+        out[b] = float(np.sum(m[nz] * r64[b][nz]))
+    return out, logz, flags
+
+
 def chain_score(pot, z, lengths=None):
     """Score(z) = Σ_{t < len-1} l[t, z_t, z_{t+1}], fp64 (exact for fp32
     inputs up to rounding of the sum).  z [B, N] int; a label outside [0, C) on a used

@@ -107,6 +107,19 @@ def entropy(pot_seq, n: int) -> float:
     return -math.fsum((p * np.log(p)).tolist())
 
 
+def expectation(pot_seq, r_seq, n: int) -> float:
+    """E_p[Σ_t r_t[z_t][z_{t+1}]] = Σ_z p(z) Σ_t r_t[z_t][z_{t+1}] by enumeration (Table 2
+    'Exp.'), structures with p = 0 omitted."""
+    Z, p = probabilities(pot_seq, n)
+    r = np.asarray(r_seq, np.float64)
+    keep = p > 0
+    Z, p = Z[keep], p[keep]
+    f = np.zeros(len(Z))
+    for t in range(n - 1):
+        f += r[t, Z[:, t], Z[:, t + 1]]
+    return math.fsum((p * f).tolist())
+
+
 def kbest(pot_seq, n: int, K: int) -> tuple[np.ndarray, np.ndarray]:
     """The first K labelings in the order (Score desc, then reverse-lexicographic asc:
     z_{n-1} first) by sorting the enumeration — the definition of the K-Max result."""

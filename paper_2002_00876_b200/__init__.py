@@ -150,6 +150,27 @@ def entropy(pot: torch.Tensor, lengths=None, ws: Workspace | None = None,
     return H, marg, logz, flags
 
 
+def expectation(pot: torch.Tensor, r: torch.Tensor, lengths=None, ws: Workspace | None = None,
+                out: torch.Tensor | None = None):
+    """E_p[Σ_p r_p z_p] = Σ mu·r of an additive feature r (same shape as pot; Table 2 'Exp.',
+    P:207): (E [B], marg, logZ, flags)."""
+    L = _lib.load()
+    ch = _chain(pot, lengths)
+    if r.shape != pot.shape or r.dtype != torch.float32 or r.device != pot.device:
+        raise ValueError("expectation: r must be a float32 tensor shaped and placed like pot")
+    r = r.contiguous()
+    B = pot.shape[0]
+    marg = out if out is not None else torch.empty_like(pot)
+    logz = torch.empty(B, dtype=torch.float32, device=pot.device)
+    ev = torch.empty(B, dtype=torch.float32, device=pot.device)
+    flags = torch.empty(B, dtype=torch.int32, device=pot.device)
+    wp, wn = _ws(pot, ch, _lib.TS_OP_EXPECTATION, _lib.TS_LOG, ws)
+    _lib.check(L.ts_expectation(ctypes.byref(ch), r.data_ptr(), marg.data_ptr(), logz.data_ptr(),
+                                ev.data_ptr(), flags.data_ptr(), wp, wn, _stream(pot.device)),
+               "ts_expectation")
+    return ev, marg, logz, flags
+
+
 def log_prob(pot: torch.Tensor, z: torch.Tensor, lengths=None, logz: torch.Tensor | None = None):
     """log p(z) = Score(z) - A for labellings z [B, N] int32; with logz=None the
     partition is computed first (ts_logpartition)."""

@@ -14,6 +14,7 @@ LIB_PATH = os.path.join(_HERE, "libts_b200.so")
 TS_LOG, TS_MAX = 0, 1
 TS_OP_LOGZ, TS_OP_MARG, TS_OP_VITERBI, TS_OP_MARG_HOST, TS_OP_SEGMENT = 0, 1, 2, 3, 4
 TS_OP_ENTROPY, TS_OP_SAMPLE, TS_OP_SEGMENT_VITERBI, TS_OP_KBEST = 5, 6, 7, 8
+TS_OP_EXPECTATION = 9
 TS_F_EMPTY, TS_F_NONFINITE, TS_F_BADLEN = 1, 2, 4
 STATUS = {0: "TS_OK", 1: "TS_E_INVALID", 2: "TS_E_UNSUPPORTED", 3: "TS_E_WORKSPACE",
           4: "TS_E_CUDA"}
@@ -22,7 +23,7 @@ STATUS = {0: "TS_OK", 1: "TS_E_INVALID", 2: "TS_E_UNSUPPORTED", 3: "TS_E_WORKSPA
 SYMBOLS = ("ts_workspace_bytes", "ts_logpartition", "ts_marginals", "ts_viterbi",
            "ts_marginals_host", "ts_segment_summary_bytes", "ts_segment_summary",
            "ts_segment_finish", "ts_set_plan_chunk", "ts_get_plan_chunk", "ts_set_small_cluster",
-           "ts_set_tiny", "ts_entropy", "ts_log_prob", "ts_sample",
+           "ts_set_tiny", "ts_entropy", "ts_expectation", "ts_log_prob", "ts_sample",
            "ts_segment_viterbi_summary_bytes", "ts_segment_viterbi_summary",
            "ts_segment_viterbi_maps", "ts_segment_viterbi_finish",
            "ts_kbest_workspace_bytes", "ts_kbest", "ts_semimarkov_workspace_bytes",
@@ -69,6 +70,7 @@ def load():
     L.ts_segment_summary.argtypes = [CH, I64, I64, INT, P, P, SZ, P]
     L.ts_segment_finish.argtypes = [CH, I64, I64, INT, INT, INT, P, P, P, P, P, SZ, P]
     L.ts_entropy.argtypes = [CH, P, P, P, P, P, SZ, P]
+    L.ts_expectation.argtypes = [CH, P, P, P, P, P, P, SZ, P]
     L.ts_semimarkov_workspace_bytes.argtypes = [CH, I64]
     L.ts_semimarkov_workspace_bytes.restype = SZ
     L.ts_semimarkov.argtypes = [CH, I64, P, P, P, P, SZ, P]
@@ -83,7 +85,7 @@ def load():
     L.ts_log_prob.argtypes = [CH, P, P, P, P]
     L.ts_sample.argtypes = [CH, P, I64, P, P, P, P, SZ, P]
     for f in ("ts_logpartition", "ts_marginals", "ts_viterbi", "ts_marginals_host",
-              "ts_segment_summary", "ts_segment_finish", "ts_entropy", "ts_log_prob",
+              "ts_segment_summary", "ts_segment_finish", "ts_entropy", "ts_expectation", "ts_log_prob",
               "ts_sample", "ts_segment_viterbi_summary", "ts_segment_viterbi_maps",
               "ts_segment_viterbi_finish", "ts_kbest", "ts_semimarkov"):
         getattr(L, f).restype = INT

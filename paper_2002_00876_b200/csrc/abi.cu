@@ -643,7 +643,8 @@ TS_API size_t ts_workspace_bytes(const ts_chain* c, int op, ts_semiring s) {
   }
   if (op == TS_OP_KBEST) return 0;  // use ts_kbest_workspace_bytes (depends on K)
   if (op == TS_OP_SEGMENT_VITERBI) return c->C <= 128 ? vseg_ws(c, nullptr, nullptr) : 0;
-  if (op == TS_OP_ENTROPY) return s == TS_LOG ? entropy_ws(c, nullptr, nullptr, nullptr) : 0;
+  if (op == TS_OP_ENTROPY || op == TS_OP_EXPECTATION)
+    return s == TS_LOG ? entropy_ws(c, nullptr, nullptr, nullptr) : 0;
   if (op == TS_OP_SAMPLE) return (s == TS_LOG && c->C <= 128) ? sample_ws(c, nullptr, nullptr, nullptr) : 0;
   if (op < TS_OP_LOGZ || op > TS_OP_VITERBI) return 0;
   return op_ws(c, op, s, nullptr, nullptr, nullptr);
@@ -824,10 +825,12 @@ TS_API ts_status ts_segment_viterbi_finish(const ts_chain* local, int64_t edge_b
   return TS_OK;
 }
 
-TS_API ts_status ts_entropy(const ts_chain* c, float* marg, float* logz, float* entropy,
-                            uint32_t* flags, void* ws, size_t ws_bytes, void* stream) {
+namespace {
+ts_status entropy_or_expectation(const ts_chain* c, const float* r, float* marg, float* logz,
+                                 float* out, uint32_t* flags, void* ws, size_t ws_bytes,
+                                 void* stream) {
   if (!chain_ok(c) || (c->N > 1 && !marg) || (marg && !aligned(marg, 16)) || !logz ||
-      !aligned(logz, 4) || !entropy || !aligned(entropy, 4) || (flags && !aligned(flags, 4)))
+      !aligned(logz, 4) || !out || !aligned(out, 4) || (flags && !aligned(flags, 4)))
     return TS_E_INVALID;
   if (!device_ok()) return TS_E_UNSUPPORTED;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -835,8 +838,8 @@ TS_API ts_status ts_entropy(const ts_chain* c, float* marg, float* logz, float* 
   double* partial = nullptr;
   const size_t need = entropy_ws(c, ws, &mpart, &partial);
   if (ws_bytes < need || !ws || !aligned(ws, kAlign)) return TS_E_WORKSPACE;
-  ts_status r = run_log(c, marg, logz, flags, ws, mpart, st);
-  if (r != TS_OK) return r;
+  ts_status st_r = run_log(c, marg, logz, flags, ws, mpart, st);
+  if (st_r != TS_OK) return st_r;
   const int n = t_launches;
   const char* k = t_kernel;
   DistArgs d{};
@@ -848,14 +851,28 @@ TS_API ts_status ts_entropy(const ts_chain* c, float* marg, float* logz, float* 
   d.marg = marg;
   d.logz = logz;
   d.flags = flags;
-  d.out = entropy;
+  d.out = out;
+  d.r = r;
   d.partial = partial;
-  r = cuda_status(launch_entropy(d, st));
-  if (r == TS_OK) {
+  st_r = cuda_status(launch_entropy(d, st));
+  if (st_r == TS_OK) {
     t_launches = n + 2;
     t_kernel = k;
   }
-  return r;
+  return st_r;
+}
+}  // namespace
+
+TS_API ts_status ts_entropy(const ts_chain* c, float* marg, float* logz, float* entropy,
+                            uint32_t* flags, void* ws, size_t ws_bytes, void* stream) {
+  return entropy_or_expectation(c, nullptr, marg, logz, entropy, flags, ws, ws_bytes, stream);
+}
+
+TS_API ts_status ts_expectation(const ts_chain* c, const float* r, float* marg, float* logz,
+                                float* out, uint32_t* flags, void* ws, size_t ws_bytes,
+                                void* stream) {
+  if (!r || !aligned(r, 16)) return TS_E_INVALID;
+  return entropy_or_expectation(c, r, marg, logz, out, flags, ws, ws_bytes, stream);
 }
 
 TS_API ts_status ts_log_prob(const ts_chain* c, const int32_t* z, const float* logz, float* out,

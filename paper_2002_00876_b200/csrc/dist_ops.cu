@@ -6,6 +6,10 @@
 //              stage deterministic reduction over the marginals the hot path just wrote:
 //              grid (B, S) slices accumulate fp64 partials, one CTA per sequence sums them in
 //              slice order.  Terms with mu = 0 are skipped (0 * -inf masks).
+//  * expectation: E_p[Σ_p r_p z_p] = Σ_{t,i,j} mu[b,t,i,j] r[b,t,i,j] for a caller-given
+//              additive feature r (Table 2 'Exp.' row; the expectation semiring's
+//              moment over all structures equals this sum by linearity): the same
+//              two-stage reduction with r in place of l, out = the sum.
 //  * score:    Score_b(z) = Σ_{t < len-1} l[b,t,z_t,z_{t+1}], fp64; log_prob =
 //              Score - A.
 //  * sampling: forward-filtering backward-sampling.  The forward node vectors alpha_hat
@@ -36,7 +40,7 @@ __device__ __forceinline__ double block_sum_d(double v, double* red) {
 }
 }  // namespace
 
-// partial[b][s] = Σ mu * l over edges [s*Ls, min((s+1)*Ls, Eb)) of sequence b
+// partial[b][s] = Σ mu * l (expectation: mu * r) over edges [s*Ls, min((s+1)*Ls, Eb)) of sequence b
 __global__ void __launch_bounds__(kRedThreads) entropy_partial_kernel(DistArgs a) {
   __shared__ double red[kRedThreads / 32];
   const int64_t b = blockIdx.x, s = blockIdx.y;
@@ -47,7 +51,7 @@ __global__ void __launch_bounds__(kRedThreads) entropy_partial_kernel(DistArgs a
   double acc = 0.0;
   if (t0 < t1) {
     const float* mu = a.marg + (b * E + t0) * CC;
-    const float* l = a.pot + (b * E + t0) * CC;
+    const float* l = (a.r ? a.r : a.pot) + (b * E + t0) * CC;
     const int64_t n = (t1 - t0) * CC;
     if ((CC & 3) == 0) {
       const float4* mu4 = reinterpret_cast<const float4*>(mu);
@@ -75,7 +79,7 @@ __global__ void entropy_final_kernel(DistArgs a, int S) {
   for (int s = 0; s < S; ++s) sum += a.partial[b * S + s];  // slice order: deterministic
   const float lz = a.logz[b];
   const bool bad = (a.flags && a.flags[b] != 0) || !(lz > -INFINITY && lz < INFINITY);
-  a.out[b] = bad ? qnan() : (float)((double)lz - sum);
+  a.out[b] = bad ? qnan() : (float)(a.r ? sum : (double)lz - sum);
 }
 
 // Score(z) (and log_prob = Score - logz when logz is given), one CTA per sequence.

@@ -157,7 +157,8 @@ struct DistArgs {
   const float* pot;
   const int32_t* lengths;
   int64_t B, N, C;
-  const float* marg;       // entropy: marginals [B][N-1][C][C]
+  const float* marg;       // entropy / expectation: marginals [B][N-1][C][C]
+  const float* r;          // expectation: additive feature [B][N-1][C][C] (NULL: entropy)
   const float* logz;       // [B] (entropy: required; score: NULL -> Score(z))
   const uint32_t* flags;   // [B] or NULL
   float* out;              // [B] entropy / log_prob

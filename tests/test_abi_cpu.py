@@ -110,6 +110,10 @@ def test_next_row_entry_points_validate_before_the_device():
     assert L.ts_entropy(ctypes.byref(ch), None, A, A, None, None, 0, None) == 1
     assert L.ts_entropy(ctypes.byref(ch), A, None, A, None, None, 0, None) == 1
     assert L.ts_entropy(ctypes.byref(ch), A, A, None, None, None, 0, None) == 1
+    # expectation: the feature r is required too (and 16-byte aligned)
+    assert L.ts_expectation(ctypes.byref(ch), None, A, A, A, None, None, 0, None) == 1
+    assert L.ts_expectation(ctypes.byref(ch), A + 4, A, A, A, None, None, 0, None) == 1
+    assert L.ts_expectation(ctypes.byref(ch), A, None, A, A, None, None, 0, None) == 1
     # log_prob: z and out required
     assert L.ts_log_prob(ctypes.byref(ch), None, None, A, None) == 1
     assert L.ts_log_prob(ctypes.byref(ch), A, None, None, None) == 1
@@ -143,6 +147,8 @@ def test_next_row_workspace_sizes():
     L = _lib.load()
     ch = _chain(B=4, N=100, C=20)
     assert L.ts_workspace_bytes(ctypes.byref(ch), _lib.TS_OP_ENTROPY, _lib.TS_LOG) >= 4 * 8
+    assert (L.ts_workspace_bytes(ctypes.byref(ch), _lib.TS_OP_EXPECTATION, _lib.TS_LOG) ==
+            L.ts_workspace_bytes(ctypes.byref(ch), _lib.TS_OP_ENTROPY, _lib.TS_LOG))
     assert L.ts_workspace_bytes(ctypes.byref(ch), _lib.TS_OP_SAMPLE, _lib.TS_LOG) >= 4 * 100 * 20 * 4
     assert L.ts_workspace_bytes(ctypes.byref(ch), _lib.TS_OP_SEGMENT_VITERBI,
                                 _lib.TS_MAX) >= 4 * 99 * 20

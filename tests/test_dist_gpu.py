@@ -1,5 +1,5 @@
 """GPU parity of the distribution properties (§3
-P:113-123): entropy, log_prob / score and FFBS sampling through the C ABI, against the
+P:113-123, Table 2): entropy, expectation, log_prob / score and FFBS sampling through the C ABI, against the
 fp64 oracle (oracle.chain_entropy / chain_log_prob / ffbs_sample, pinned in
 tests/test_oracle_dist_pins.py).
 
@@ -74,6 +74,42 @@ def test_entropy_closed_form_uniform(dev):
     N, C = 25, 20
     H, _, _, _ = tsb.entropy(torch.zeros((4, N - 1, C, C), device=dev))
     assert np.allclose(H.cpu().numpy(), N * math.log(C), rtol=1e-6)
+
+
+@pytest.mark.parametrize("B,N,C", SHAPES)
+def test_expectation_parity(dev, B, N, C):
+    """Table 2 'Exp.': Σ mu·r against oracle.chain_expectation (pinned by
+    enumeration); gate |dE| <= 1e-5 * max(1, Σ|mu·r|-scale) with the scale = len - 1."""
+    pot = tsgen.potentials(B, N, C, seed=4500 + N + C)
+    r = np.random.default_rng(N + 3 * C).standard_normal(pot.shape).astype(np.float32)
+    ref, lz_ref, fl_ref = oracle.chain_expectation(pot, r, threads=8)
+    ev, marg, lz, fl = tsb.expectation(_dev(pot, dev), _dev(r, dev))
+    check_logz(lz.cpu().numpy(), lz_ref)
+    assert (fl.cpu().numpy().astype(np.uint32) == fl_ref).all()
+    _check_rel(ev.cpu().numpy(), ref, np.full(B, float(N - 1)))
+
+
+def test_expectation_lengths_flags_closed_form(dev):
+    B, N, C = 6, 40, 20
+    pot = tsgen.tagging_potentials(B, N, C, seed=12, mask_frac=0.2)
+    lengths = tsgen.random_lengths(B, N, C)
+    lengths[0], lengths[1] = 1, N
+    pot[2] = -np.inf
+    lengths[2] = N
+    lengths[3] = 0
+    ones = np.ones_like(pot)
+    ref, _, fl_ref = oracle.chain_expectation(pot, ones, lengths, threads=8)
+    ev, _, _, fl = tsb.expectation(_dev(pot, dev), _dev(ones, dev), _dev(lengths, dev))
+    assert (fl.cpu().numpy().astype(np.uint32) == fl_ref).all()
+    ev = ev.cpu().numpy()
+    _check_rel(ev, ref, np.full(B, float(N)))
+    for b in (0, 1, 4, 5):   # r = 1 counts the edges: len - 1
+        assert abs(ev[b] - (lengths[b] - 1)) <= 1e-5 * max(1, lengths[b]), (b, ev[b])
+    # r = l: E_p[Score] = A - H (P:122)
+    pot = tsgen.potentials(4, 25, 20, seed=2)
+    H, _, lz, _ = tsb.entropy(_dev(pot, dev))
+    es, _, _, _ = tsb.expectation(_dev(pot, dev), _dev(pot, dev))
+    assert float((es.double() - (lz.double() - H.double())).abs().max()) <= 1e-5 * float(lz.abs().max())
 
 
 @pytest.mark.parametrize("B,N,C", SHAPES)
@@ -176,10 +212,11 @@ def test_new_ops_deterministic_bitwise(dev):
     runs = []
     for _ in range(2):
         H, _, _, _ = tsb.entropy(pot)
+        ex, _, _, _ = tsb.expectation(pot, pot * 0.5 + 1.0)
         lp = tsb.log_prob(pot, z)
         zz, _, _ = tsb.sample(pot, u)
         kp, ks, _ = tsb.kbest(pot, 5)
         mg, lz, _ = tsb.semimarkov(sm)
-        runs.append([x.clone() for x in (H, lp, zz, kp, ks, mg, lz)])
+        runs.append([x.clone() for x in (H, ex, lp, zz, kp, ks, mg, lz)])
     for a, b in zip(*runs):
         assert torch.equal(a, b)

@@ -1,5 +1,5 @@
 """Pins for the oracle's distribution properties (entropy,
-density / log_prob, forward-filtering backward-sampling; §3, Table 2
+expectation of an additive feature, density / log_prob, forward-filtering backward-sampling; §3, Table 2
 P:202-206) against things other than the oracle itself: brute-force enumeration of
 every labelling (P:149 footnote), closed forms of the definitions, and exact sampling
 frequencies.  A plausible bug (sign of the expectation term, conditioning on the wrong
@@ -63,6 +63,61 @@ def test_entropy_flags():
     H, _, flags = oracle.chain_entropy(pot)
     assert math.isnan(H[0]) and math.isnan(H[1]) and not math.isnan(H[2])
     assert flags[0] == oracle.F_EMPTY and flags[1] == oracle.F_NONFINITE
+
+
+@pytest.mark.parametrize("B,N,C", CASES)
+def test_expectation_matches_enumeration(B, N, C):
+    """Table 2 'Exp.': E_p[Σ_t r_t(z_t, z_{t+1})] against Σ_z p(z) f(z)."""
+    pot = tsgen.potentials(B, N, C, seed=2500 + 7 * N + C, s=8)
+    r = np.random.default_rng(N * C).standard_normal(pot.shape).astype(np.float32)
+    ev, _, flags = oracle.chain_expectation(pot, r)
+    assert (flags == 0).all()
+    for b in range(B):
+        assert abs(ev[b] - brute.expectation(pot[b], r[b], N)) <= 1e-10 * max(1.0, abs(ev[b]))
+
+
+def test_expectation_masked_lengths_and_garbage_at_masks():
+    B, N, C = 4, 6, 3
+    pot = tsgen.tagging_potentials(B, N, C, seed=9, mask_frac=0.3)
+    lengths = np.array([6, 4, 1, 5], dtype=np.int32)
+    r = np.random.default_rng(1).standard_normal(pot.shape).astype(np.float32)
+    r2 = r.copy()
+    r2[np.isneginf(pot)] = np.nan            # r at masked parts (mu = 0) never matters
+    r2[1, 3:] = np.inf                       # nor beyond the sequence
+    ev, _, _ = oracle.chain_expectation(pot, r, lengths)
+    ev2, _, _ = oracle.chain_expectation(pot, r2, lengths)
+    for b in range(B):
+        n = int(lengths[b])
+        assert abs(ev[b] - brute.expectation(pot[b], r[b], n)) <= 1e-10 * max(1.0, abs(ev[b]))
+    assert np.array_equal(ev, ev2)
+    assert ev[2] == 0.0                      # len 1: no edges
+
+
+def test_expectation_closed_forms():
+    # r = 1: every labelling has len-1 edges
+    pot = tsgen.potentials(2, 30, 7, seed=4)
+    ev, _, _ = oracle.chain_expectation(pot, np.ones_like(pot), np.array([30, 11], np.int32))
+    assert ev[0] == pytest.approx(29.0, rel=1e-12) and ev[1] == pytest.approx(10.0, rel=1e-12)
+    # separable l[t,i,j] = phi_t[j], r[t,i,j] = psi_t[j]: z_{t+1} ~ softmax(phi_t) -> Σ_t <p_t, psi_t>
+    rng = np.random.default_rng(8)
+    N, C = 40, 6
+    phi = rng.standard_normal((N - 1, C)).astype(np.float32)
+    psi = rng.standard_normal((N - 1, C)).astype(np.float32)
+    pot = np.broadcast_to(phi[:, None, :], (N - 1, C, C)).astype(np.float32)[None]
+    r = np.broadcast_to(psi[:, None, :], (N - 1, C, C)).astype(np.float32)[None]
+    ev, _, _ = oracle.chain_expectation(pot, r)
+    ref = 0.0
+    for t in range(N - 1):
+        p = np.exp(phi[t].astype(np.float64) - phi[t].max())
+        ref += float(np.sum(p / p.sum() * psi[t]))
+    assert ev[0] == pytest.approx(ref, rel=1e-12)
+    # an indicator feature picks out one marginal: E[z_p] = p(z_p = 1) (P:181-183, Table 2)
+    pot = tsgen.potentials(1, 5, 3, seed=6, s=8)
+    r = np.zeros_like(pot)
+    r[0, 2, 1, 0] = 1.0
+    ev, _, _ = oracle.chain_expectation(pot, r)
+    Z, p = brute.probabilities(pot[0], 5)
+    assert ev[0] == pytest.approx(float(p[(Z[:, 2] == 1) & (Z[:, 3] == 0)].sum()), abs=1e-12)
 
 
 @pytest.mark.parametrize("B,N,C", CASES)
