@@ -125,6 +125,19 @@ TS_API ts_status ts_viterbi(const ts_chain *c, int32_t *path, float *score, uint
  * the sequence) out or NULL; flags as ts_marginals.  C <= 256.
  * ws: ts_semimarkov_workspace_bytes(c, K) bytes, 256-byte aligned. */
 TS_API size_t ts_semimarkov_workspace_bytes(const ts_chain *c, int64_t K);
+/* Semi-Markov Viterbi (the max semiring, over the segmentations of R17):
+ * the best labelled segmentation, canonical by reading R18 (backpointers = the first
+ * (k asc, c' asc) maximiser, end label = the smallest arg-max: the lexicographically
+ * smallest (y_m, k_m, y_{m-1}, ..., y_0) read from the end).  c->pot [B][N-1][K][C][C] as
+ * ts_semimarkov, 1 <= K <= 16, C <= 256.  seg [B][N] int32 out: the label at each segment
+ * boundary node (0, p_1, ..., len-1), -1 at interior nodes, beyond len and for flagged
+ * sequences; score [B] fp32 out (fp32 adds: equal to the fp64 oracle on dyadic inputs;
+ * -inf EMPTY, NaN NONFINITE / BADLEN); flags [B] out or NULL.
+ * ws: ts_semimarkov_viterbi_workspace_bytes(c, K) bytes (uint16 backpointers [B][N][C]),
+ * 256-byte aligned. */
+TS_API size_t ts_semimarkov_viterbi_workspace_bytes(const ts_chain *c, int64_t K);
+TS_API ts_status ts_semimarkov_viterbi(const ts_chain *c, int64_t K, int32_t *seg, float *score,
+                                       uint32_t *flags, void *ws, size_t ws_bytes, void *stream);
 TS_API ts_status ts_semimarkov(const ts_chain *c, int64_t K, float *marg, float *logz,
                                uint32_t *flags, void *ws, size_t ws_bytes, void *stream);
 

@@ -421,3 +421,63 @@ def semimarkov_marginals(pot, lengths=None, want_marg: bool = True):
                         x = al[n][:, None] + pot64[b, n, k - 1] + be[n + k][None, :] - A
                     marg[b, n, k - 1] = np.where(np.isfinite(x), np.exp(x), 0.0)
     return logz, marg, flags
+
+
+def semimarkov_viterbi(pot, lengths=None):
+    """Semi-Markov Viterbi: the max semiring over the labelled segmentations
+    of reading R17:
+        delta_0[c] = 0,  delta_p[c] = max_{k <= min(K,p), c'} delta_{p-k}[c'] + l[p-k, k-1, c', c]
+    backpointer of (p, c) = the first (k, c') in (k asc, c' asc) order attaining the max
+    (strict >), end label = the smallest c attaining max_c delta_E[c] (reading R18: the
+    labelled segmentation that is lexicographically smallest in (y_m, k_m, y_{m-1}, ..., y_0)
+    read from the end).  fp64.
+    -> (seg [B, N] int32: the label at every segment boundary node, -1 at interior nodes,
+        beyond len and for flagged sequences; score [B] f64; flags as semimarkov_marginals
+        with EMPTY -> score -inf)."""
+    pot64 = np.asarray(pot, dtype=np.float64)
+    B, E, K, C, _ = pot64.shape
+    N = E + 1
+    seg = np.full((B, N), -1, dtype=np.int32)
+    score = np.empty(B)
+    flags = np.zeros(B, dtype=np.uint32)
+    for b in range(B):
+        n_b = N if lengths is None else int(lengths[b])
+        if n_b < 1 or n_b > N:
+            score[b] = math.nan
+            flags[b] = F_BADLEN
+            continue
+        Eb = n_b - 1
+        used = np.zeros((E, K), bool)
+        for n in range(Eb):
+            used[n, :min(K, Eb - n)] = True
+        if np.any(~np.isfinite(pot64[b][used]) & ~(pot64[b][used] == -np.inf)):
+            score[b] = math.nan
+            flags[b] = F_NONFINITE
+            continue
+        dl = np.full((Eb + 1, C), -np.inf)
+        dl[0] = 0.0
+        bk = np.zeros((Eb + 1, C), dtype=np.int64)
+        bc = np.zeros((Eb + 1, C), dtype=np.int64)
+        for p in range(1, Eb + 1):
+            for k in range(1, min(K, p) + 1):
+                cand = dl[p - k][:, None] + pot64[b, p - k, k - 1]    # [c', c]
+                arg = np.argmax(cand, axis=0)                         # first c' on ties
+                val = cand[arg, np.arange(C)]
+                better = val > dl[p]                                  # strict: earlier k wins
+                dl[p] = np.where(better, val, dl[p])
+                bk[p] = np.where(better, k, bk[p])
+                bc[p] = np.where(better, arg, bc[p])
+        best = float(np.max(dl[Eb]))
+        if best == -np.inf:
+            score[b] = -np.inf
+            flags[b] = F_EMPTY
+            continue
+        c = int(np.argmax(dl[Eb]))
+        score[b] = best
+        p = Eb
+        while p > 0:
+            seg[b, p] = c
+            k, c = int(bk[p, c]), int(bc[p, c])
+            p -= k
+        seg[b, 0] = c
+    return seg, score, flags

@@ -148,6 +148,35 @@ def segmentations(E: int, K: int):
     return out
 
 
+def semimarkov_argmax(pot_seq, n: int):
+    """The canonical best labelled segmentation by enumeration (reading R18): among the
+    maximisers of Score (R17), the one whose key (y_m, k_m, y_{m-1}, k_{m-1}, ..., k_1, y_0)
+    — read from the end — is lexicographically smallest.  -> (seg [n] int32 as
+    oracle.semimarkov_viterbi, score); score -inf and seg all -1 when nothing is finite."""
+    pot = np.asarray(pot_seq, dtype=np.float64)
+    _, K, C, _ = pot.shape
+    E = n - 1
+    best, best_key, best_seg = -math.inf, None, None
+    for bnd in segmentations(E, K):
+        m = len(bnd) - 1
+        for ys in np.ndindex(*([C] * (m + 1))):
+            sc = sum(pot[bnd[s - 1], bnd[s] - bnd[s - 1] - 1, ys[s - 1], ys[s]]
+                     for s in range(1, m + 1)) if m else 0.0
+            if sc == -math.inf:
+                continue
+            key = []
+            for s in range(m, 0, -1):
+                key += [ys[s], bnd[s] - bnd[s - 1]]
+            key.append(ys[0])
+            if sc > best or (sc == best and key < best_key):
+                best, best_key, best_seg = sc, key, (bnd, ys)
+    seg = np.full(n, -1, dtype=np.int32)
+    if best_seg is not None:
+        for p, y in zip(*best_seg):
+            seg[p] = y
+    return seg, best
+
+
 def semimarkov(pot_seq, n: int):
     """(A, mu) of a semi-Markov chain by enumerating every segmentation x labelling (reading
     R17): Score = Σ_s l[p_{s-1}, p_s - p_{s-1} - 1, y_{s-1}, y_s]."""

@@ -358,6 +358,25 @@ def semimarkov(pot: torch.Tensor, lengths=None, want_marg: bool = True,
     return marg, logz, flags
 
 
+def semimarkov_viterbi(pot: torch.Tensor, lengths=None, ws: Workspace | None = None):
+    """Semi-Markov Viterbi (readings R17/R18): pot [B, N-1, K, C, C] -> (seg [B, N] int32:
+    the label at each segment boundary node, -1 elsewhere; score [B]; flags [B])."""
+    L = _lib.load()
+    assert pot.dim() == 5 and pot.is_contiguous()
+    B, E, K, C, _ = pot.shape
+    ch = _lib.ts_chain(B, E + 1, C, pot.data_ptr(),
+                       lengths.data_ptr() if lengths is not None else None)
+    seg = torch.empty((B, E + 1), dtype=torch.int32, device=pot.device)
+    score = torch.empty(B, dtype=torch.float32, device=pot.device)
+    flags = torch.empty(B, dtype=torch.int32, device=pot.device)
+    need = int(L.ts_semimarkov_viterbi_workspace_bytes(ctypes.byref(ch), int(K)))
+    ws = ws or Workspace.get(pot.device)
+    _lib.check(L.ts_semimarkov_viterbi(ctypes.byref(ch), int(K), seg.data_ptr(), score.data_ptr(),
+                                       flags.data_ptr(), ws.ptr(need), need, _stream(pot.device)),
+               "ts_semimarkov_viterbi")
+    return seg, score, flags
+
+
 def kbest(pot: torch.Tensor, K: int, lengths=None, ws: Workspace | None = None):
     """The K best labelings (Table 2 'K-Max'; order: score desc, then reverse-
     lexicographic): (paths [B, K, N] int32, scores [B, K], flags [B])."""

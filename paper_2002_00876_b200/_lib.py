@@ -27,7 +27,7 @@ SYMBOLS = ("ts_workspace_bytes", "ts_logpartition", "ts_marginals", "ts_viterbi"
            "ts_segment_viterbi_summary_bytes", "ts_segment_viterbi_summary",
            "ts_segment_viterbi_maps", "ts_segment_viterbi_finish",
            "ts_kbest_workspace_bytes", "ts_kbest", "ts_semimarkov_workspace_bytes",
-           "ts_semimarkov",
+           "ts_semimarkov", "ts_semimarkov_viterbi_workspace_bytes", "ts_semimarkov_viterbi",
            "ts_set_meet", "ts_set_viterbi_split", "ts_set_host_graphs",
            "ts_host_alloc", "ts_host_free", "ts_set_tc_summary", "ts_get_tc_summary",
            "ts_last_launch_count", "ts_last_kernel", "ts_status_str", "ts_version")
@@ -74,6 +74,9 @@ def load():
     L.ts_semimarkov_workspace_bytes.argtypes = [CH, I64]
     L.ts_semimarkov_workspace_bytes.restype = SZ
     L.ts_semimarkov.argtypes = [CH, I64, P, P, P, P, SZ, P]
+    L.ts_semimarkov_viterbi_workspace_bytes.argtypes = [CH, I64]
+    L.ts_semimarkov_viterbi_workspace_bytes.restype = SZ
+    L.ts_semimarkov_viterbi.argtypes = [CH, I64, P, P, P, P, SZ, P]
     L.ts_kbest_workspace_bytes.argtypes = [CH, I64]
     L.ts_kbest_workspace_bytes.restype = SZ
     L.ts_kbest.argtypes = [CH, I64, P, P, P, P, SZ, P]
@@ -87,7 +90,7 @@ def load():
     for f in ("ts_logpartition", "ts_marginals", "ts_viterbi", "ts_marginals_host",
               "ts_segment_summary", "ts_segment_finish", "ts_entropy", "ts_expectation", "ts_log_prob",
               "ts_sample", "ts_segment_viterbi_summary", "ts_segment_viterbi_maps",
-              "ts_segment_viterbi_finish", "ts_kbest", "ts_semimarkov"):
+              "ts_segment_viterbi_finish", "ts_kbest", "ts_semimarkov", "ts_semimarkov_viterbi"):
         getattr(L, f).restype = INT
     L.ts_set_plan_chunk.argtypes = [I64]
     L.ts_set_plan_chunk.restype = None

@@ -680,6 +680,38 @@ TS_API ts_status ts_semimarkov(const ts_chain* c, int64_t K, float* marg, float*
   return r;
 }
 
+TS_API size_t ts_semimarkov_viterbi_workspace_bytes(const ts_chain* c, int64_t K) {
+  if (!chain_ok(c) || K < 1 || K > 16) return 0;
+  return align_up(sizeof(uint16_t) * (size_t)(c->B * c->N * c->C));
+}
+
+TS_API ts_status ts_semimarkov_viterbi(const ts_chain* c, int64_t K, int32_t* seg, float* score,
+                                       uint32_t* flags, void* ws, size_t ws_bytes, void* stream) {
+  if (!chain_ok(c) || K < 1 || K > 16 || !seg || !aligned(seg, 4) || !score ||
+      !aligned(score, 4) || (flags && !aligned(flags, 4)))
+    return TS_E_INVALID;
+  if (!device_ok()) return TS_E_UNSUPPORTED;
+  const size_t need = ts_semimarkov_viterbi_workspace_bytes(c, K);
+  if (ws_bytes < need || !ws || !aligned(ws, kAlign)) return TS_E_WORKSPACE;
+  SemiVitArgs a{};
+  a.pot = c->pot;
+  a.lengths = c->lengths;
+  a.B = c->B;
+  a.N = c->N;
+  a.C = c->C;
+  a.K = K;
+  a.seg = seg;
+  a.score = score;
+  a.flags = flags;
+  a.bp = static_cast<uint16_t*>(ws);
+  ts_status r = cuda_status(launch_semimarkov_viterbi(a, static_cast<cudaStream_t>(stream)));
+  if (r == TS_OK) {
+    t_launches = 1;
+    t_kernel = "semimarkov_viterbi_kernel";
+  }
+  return r;
+}
+
 TS_API size_t ts_kbest_workspace_bytes(const ts_chain* c, int64_t K) {
   if (!chain_ok(c) || K < 1 || K > 16) return 0;
   const int64_t E = c->N - 1 > 0 ? c->N - 1 : 1;

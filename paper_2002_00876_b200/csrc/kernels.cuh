@@ -191,6 +191,18 @@ struct SemiArgs {
   double* zbuf;            // [B] logZ in fp64
 };
 cudaError_t launch_semimarkov(const SemiArgs& a, cudaStream_t st);
+// semi-Markov Viterbi (reading R18): seg [B][N] int32 out, score [B] out, bp [B][N][C] uint16
+// workspace ((k-1) * C + c'), flags as the other entry points
+struct SemiVitArgs {
+  const float* pot;        // [B][N-1][K][C][C]
+  const int32_t* lengths;
+  int64_t B, N, C, K;
+  int32_t* seg;
+  float* score;
+  uint32_t* flags;
+  uint16_t* bp;
+};
+cudaError_t launch_semimarkov_viterbi(const SemiVitArgs& a, cudaStream_t st);
 
 // ---- K-best Viterbi (kbest.cu) -------------------------------------------
 struct KbestArgs {

@@ -186,4 +186,128 @@ cudaError_t launch_semimarkov(const SemiArgs& a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// ---- semi-Markov Viterbi (max semiring over R17 segmentations; reading R18) -------------
+//   delta_p[c] = max_{k <= min(K,p), c'} delta_{p-k}[c'] + l[p-k, k-1, c', c]
+// thread c owns label c; candidates are scanned in (k asc, c' asc) order with a strict >, so
+// the backpointer is the first maximiser (the oracle's rule); the last K+1 delta vectors
+// live in an SMEM ring.  fp32 adds: exact (= the fp64 oracle) on dyadic inputs whose
+// partial sums fit 24 bits.  The end label is the smallest arg-max; one thread backtracks.
+__global__ void __launch_bounds__(256) semimarkov_viterbi_kernel(SemiVitArgs a) {
+  extern __shared__ __align__(16) float vsm[];
+  const int C = (int)a.C, K = (int)a.K, R = K + 1, NT = blockDim.x;
+  const int64_t N = a.N, E = N - 1, KCC = (int64_t)K * C * C;
+  const int64_t b = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  float* ring = vsm;                                    // [R][NT]
+  float* rv = ring + R * NT;                            // [8] block arg-max values
+  int* ri = reinterpret_cast<int*>(rv + 8);             // [8] block arg-max labels
+  unsigned* sflag = reinterpret_cast<unsigned*>(ri + 8);
+  const float* pb = a.pot + b * E * KCC;
+  int32_t* sg = a.seg + b * N;
+  uint16_t* bp = a.bp + b * N * C;
+  const int64_t len = seq_len(a.lengths, b, N);
+  for (int64_t p = tid; p < N; p += NT) sg[p] = -1;
+  if (len < 0) {
+    if (tid == 0) {
+      a.score[b] = qnan();
+      if (a.flags) a.flags[b] = TS_F_BADLEN;
+    }
+    return;
+  }
+  const int64_t Eb = len - 1;
+  const bool act = tid < C;
+  if (tid == 0) *sflag = 0u;
+  ring[tid] = act ? 0.f : neg_inf();                    // delta_0 = 0 (node 0 in slot 0)
+  __syncthreads();
+  bool bad = false;
+  for (int64_t p = 1; p <= Eb; ++p) {
+    float best = neg_inf();
+    int arg = 0;
+    if (act) {
+      const int kmax = (int)(p < K ? p : K);
+      for (int k = 1; k <= kmax; ++k) {
+        const float* dq = ring + ((p - k) % R) * NT;
+        const float* col = pb + (p - k) * KCC + (int64_t)(k - 1) * C * C + tid;
+        constexpr int kPf = 8;  // column values loaded per batch (independent loads in flight)
+        for (int i0 = 0; i0 < C; i0 += kPf) {
+          float lv[kPf];
+#pragma unroll
+          for (int u = 0; u < kPf; ++u) lv[u] = (i0 + u < C) ? col[(int64_t)(i0 + u) * C] : neg_inf();
+#pragma unroll
+          for (int u = 0; u < kPf; ++u) {
+            bad |= (lv[u] != lv[u]) | (lv[u] == pos_inf());
+            const float v = dq[i0 + u < C ? i0 + u : 0] + lv[u];
+            if (v > best) {
+              best = v;
+              arg = (k - 1) * C + i0 + u;
+            }
+          }
+        }
+      }
+      bp[p * C + tid] = (uint16_t)arg;
+    }
+    ring[(p % R) * NT + tid] = act ? best : neg_inf();
+    __syncthreads();
+  }
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(sflag, 1u);
+  // end label: the smallest c attaining max delta_Eb
+  float v = act ? ring[(Eb % R) * NT + tid] : neg_inf();
+  int idx = (act && v != neg_inf()) ? tid : 0x7fffffff;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, v, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+    if (ov > v || (ov == v && oi < idx)) {
+      v = ov;
+      idx = oi;
+    }
+  }
+  if (lane == 0) {
+    rv[w] = v;
+    ri[w] = idx;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    float bv = rv[0];
+    int bi = ri[0];
+    for (int q = 1; q < NT / 32; ++q)
+      if (rv[q] > bv || (rv[q] == bv && ri[q] < bi)) {
+        bv = rv[q];
+        bi = ri[q];
+      }
+    unsigned fl = 0;
+    if (*sflag) {
+      fl = TS_F_NONFINITE;
+      a.score[b] = qnan();
+    } else if (bv == neg_inf()) {
+      fl = TS_F_EMPTY;
+      a.score[b] = neg_inf();
+    } else {
+      a.score[b] = bv;
+      int c = bi;
+      int64_t p = Eb;
+      while (p > 0) {
+        sg[p] = c;
+        const int v16 = bp[p * C + c];
+        const int k = v16 / C + 1;
+        c = v16 - (k - 1) * C;
+        p -= k;
+      }
+      sg[0] = c;
+    }
+    if (a.flags) a.flags[b] = fl;
+  }
+}
+
+size_t semimarkov_viterbi_smem(int64_t C, int64_t K) {
+  const int NT = (int)(((C + 31) / 32) * 32);
+  return (size_t)(K + 1) * NT * sizeof(float) + 8 * sizeof(float) + 8 * sizeof(int) + 16;
+}
+
+cudaError_t launch_semimarkov_viterbi(const SemiVitArgs& a, cudaStream_t st) {
+  const int NT = (int)(((a.C + 31) / 32) * 32);
+  semimarkov_viterbi_kernel<<<(unsigned)a.B, NT, semimarkov_viterbi_smem(a.C, a.K), st>>>(a);
+  return cudaGetLastError();
+}
+
 }  // namespace tsb

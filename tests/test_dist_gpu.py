@@ -217,6 +217,7 @@ def test_new_ops_deterministic_bitwise(dev):
         zz, _, _ = tsb.sample(pot, u)
         kp, ks, _ = tsb.kbest(pot, 5)
         mg, lz, _ = tsb.semimarkov(sm)
-        runs.append([x.clone() for x in (H, ex, lp, zz, kp, ks, mg, lz)])
+        sg, ss, _ = tsb.semimarkov_viterbi(sm)
+        runs.append([x.clone() for x in (H, ex, lp, zz, kp, ks, mg, lz, sg, ss)])
     for a, b in zip(*runs):
         assert torch.equal(a, b)

@@ -297,3 +297,33 @@ def test_semimarkov_finite_differences_and_flags():
     assert fl[0] == oracle.F_EMPTY and lz[0] == -np.inf and (mg[0] == 0).all()
     assert fl[1] == oracle.F_NONFINITE and math.isnan(lz[1])
     assert fl[2] == 0
+
+
+@pytest.mark.parametrize("N,K,C,s", [(5, 3, 2, 1), (6, 2, 3, 1), (4, 4, 3, 0), (7, 3, 2, 2),
+                                     (1, 2, 3, 1), (2, 1, 3, 1)])
+def test_semimarkov_viterbi_matches_enumeration(N, K, C, s):
+    """Semi-Markov Viterbi (R17/R18) against the canonical enumerated argmax; coarse dyadic
+    values (2^-s grid) so ties are frequent and the tie rule is exercised."""
+    rng = np.random.default_rng(100 * N + 10 * K + C + s)
+    B = 6
+    pot = (rng.integers(-3, 4, size=(B, N - 1, K, C, C)) * 2.0 ** -s).astype(np.float32)
+    pot[1, ..., 0, :] = -np.inf if N > 1 else 0.0      # masked transitions out of label 0
+    seg, score, flags = oracle.semimarkov_viterbi(pot)
+    for b in range(B):
+        ref_seg, ref = brute.semimarkov_argmax(pot[b], N)
+        assert score[b] == ref and np.array_equal(seg[b], ref_seg), (b, seg[b], ref_seg)
+
+
+def test_semimarkov_viterbi_k1_is_chain_viterbi_and_flags():
+    pot = tsgen.potentials(4, 12, 5, seed=3, s=8)
+    lengths = np.array([12, 7, 1, 12], np.int32)
+    seg, score, flags = oracle.semimarkov_viterbi(pot[:, :, None], lengths)
+    path, sc, fl = oracle.chain_viterbi(pot, lengths)
+    assert np.array_equal(seg, path) and np.array_equal(score, sc) and (flags == fl).all()
+    bad = tsgen.potentials(4, 6, 3, seed=1)[:, :, None].repeat(2, axis=2)
+    bad[0] = -np.inf
+    bad[1, 2, 0, 0, 0] = np.nan
+    seg, score, flags = oracle.semimarkov_viterbi(bad, np.array([6, 6, 0, 6], np.int32))
+    assert list(flags[:3]) == [oracle.F_EMPTY, oracle.F_NONFINITE, oracle.F_BADLEN]
+    assert score[0] == -np.inf and math.isnan(score[1]) and math.isnan(score[2])
+    assert (seg[:3] == -1).all() and flags[3] == 0
