@@ -250,8 +250,9 @@ ts_status run_log(const ts_chain* c, float* marg, float* logz, uint32_t* flags, 
   const Plan p = log_plan(c);
   if (p.kind == PlanKind::Unsupported) {
     if (c->C > 256) return TS_E_UNSUPPORTED;
-    // long chains with 128 < C <= 256: the exact SIMT segmental kernel with K = 1 (= the
-    // linear chain, reading R17), forward and backward recursions concurrently
+    // long chains with 128 < C <= 256: forward and backward recursion CTAs concurrently
+    // (exact per-cell LSE), then a machine-wide marginal pass (fb_wide.cu); the workspace is
+    // the segmental kernel's with K = 1
     SemiArgs sa{};
     const size_t need = semi_ws(c, 1, ws, &sa);
     if (ws_bytes < need || !ws || !aligned(ws, kAlign)) return TS_E_WORKSPACE;
@@ -263,10 +264,10 @@ ts_status run_log(const ts_chain* c, float* marg, float* logz, uint32_t* flags, 
     sa.marg = marg;
     sa.logz = logz;
     sa.flags = flags;
-    ts_status r = cuda_status(launch_semimarkov(sa, st));
+    ts_status r = cuda_status(launch_fb_wide(sa, st));
     if (r == TS_OK) {
-      t_launches = 1;
-      t_kernel = "semimarkov_kernel";
+      t_launches = (marg && c->N > 1) ? 2 : 1;
+      t_kernel = "fb_wide_sweep_kernel";
     }
     return r;
   }

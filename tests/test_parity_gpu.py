@@ -99,14 +99,58 @@ def test_cfg3_reduced_elementwise(dev):
 
 @pytest.mark.parametrize("B,N,C", [(2, 70, 130), (3, 40, 200), (2, 30, 256), (2, 2, 256)])
 def test_log_semiring_wide_labels(dev, B, N, C):
-    """128 < C <= 256 on chains that do not fit one CTA: the exact SIMT segmental kernel with
-    K = 1 (reading R17 reduces to the linear chain)."""
+    """128 < C <= 256 on chains that do not fit one CTA: fb_wide (forward / backward recursion
+    CTAs with the exact per-cell LSE, then a machine-wide marginal pass)."""
     pot = tsgen.potentials(B, N, C, seed=900 + N + C)
     assert_log_parity(pot, None, dev)
     lengths = np.array([N] + [max(1, N // 3)] * (B - 1), np.int32)
     assert_log_parity(pot, lengths, dev)
     pot[0, N // 2 - 1, 3, 4] = np.nan
     assert_log_parity(pot, None, dev)
+
+
+@pytest.mark.parametrize("C", [131, 256])
+def test_log_wide_labels_masks_flags_ranges(dev, C):
+    """fb_wide (128 < C <= 256): masks, EMPTY / NONFINITE / BADLEN / len-1 rows, offsets,
+    peaked and wide-range inputs; C = 131 takes the scalar (C*C % 4 != 0) marginal path."""
+    B, N = 7, 45
+    pot = tsgen.tagging_potentials(B, N, C, seed=C, mask_frac=0.2)
+    lengths = tsgen.random_lengths(B, N, C)
+    lengths[0], lengths[1] = 1, N
+    pot[2] = -np.inf
+    lengths[2] = N
+    pot[3, 7, 2, 1] = np.inf
+    lengths[3] = N
+    lengths[4] = 0
+    lengths[5] = N + 2
+    assert_log_parity(pot, lengths, dev)
+    assert_log_parity(tsgen.large_offset_potentials(2, 30, C, seed=C), None, dev)
+    assert_log_parity(tsgen.peaked_potentials(2, 30, C, seed=C), None, dev)
+    assert_log_parity(tsgen.wide_potentials(2, 30, C, seed=C, scale=50.0), None, dev)
+
+
+def test_log_wide_cfg4_shape_full(dev):
+    """logZ + marginals at cfg4's full shape (B64 N1024 C256, the log semiring) through
+    fb_wide; oracle on sampled sequences (first, last) element by element, every sequence's
+    marginals sum to 1 per edge."""
+    cfg = tsgen.CONFIGS[4]
+    pot = torch.empty((cfg.B, cfg.E, cfg.C, cfg.C), dtype=torch.float32, device=dev)
+    tsgen.fill_torch(pot, cfg)
+    m, lz, fl = tsb.marginals(pot)
+    assert tsb.last_kernel() == "fb_wide_sweep_kernel"
+    assert (fl.cpu().numpy() == 0).all()
+    sums = m.sum(dim=(2, 3), dtype=torch.float64)
+    assert float((sums - 1).abs().max()) < 1e-4
+    lz = lz.cpu().numpy()
+    CC = cfg.C * cfg.C
+    for b in (0, cfg.B - 1):
+        idx = np.arange(b * cfg.E * CC, (b + 1) * cfg.E * CC, dtype=np.uint64)
+        pb = tsgen.values_at(cfg.seed, cfg.quantum, idx).reshape(1, cfg.E, cfg.C, cfg.C)
+        lz_ref, mg_ref, fl_ref = oracle.chain_marginals(pb, None, threads=8)
+        check_logz(lz[b:b + 1], lz_ref)
+        check_marg(m[b:b + 1].cpu().numpy(), mg_ref)
+    del pot, m
+    torch.cuda.empty_cache()
 
 
 @pytest.mark.parametrize("C", [3, 20, 64, 130, 256])

@@ -48,6 +48,7 @@ def main():
         out = torch.empty_like(pot)
         for name, fn in [("marginals", lambda: tsb.marginals(pot, out=out)),
                          ("entropy", lambda: tsb.entropy(pot, out=out)),
+                         ("expectation", lambda: tsb.expectation(pot, pot, out=out)),
                          ("log_prob", lambda: tsb.log_prob(pot, z)),
                          ("sample_k4", lambda: tsb.sample(pot, u)),
                          ("kbest_k4", lambda: tsb.kbest(pot, 4)),
@@ -62,6 +63,18 @@ def main():
     ms = timeit(lambda: tsb.semimarkov(sm), iters=args.iters)
     rows.append({"config": "semi B32 N25 K4 C20", "op": "semimarkov", "ms": ms,
                  "tokens_per_s": 32 * 25 / (ms / 1e3)})
+    ms = timeit(lambda: tsb.semimarkov_viterbi(sm), iters=args.iters)
+    rows.append({"config": "semi B32 N25 K4 C20", "op": "semimarkov_viterbi", "ms": ms,
+                 "tokens_per_s": 32 * 25 / (ms / 1e3)})
+    # wide-label log path (128 < C <= 256: exact SIMT fallback), cfg4's shape
+    cfg = tsgen.CONFIGS[4]
+    pot = torch.empty((cfg.B, cfg.E, cfg.C, cfg.C), dtype=torch.float32, device=dev)
+    tsgen.fill_torch(pot, cfg)
+    out = torch.empty_like(pot)
+    ms = timeit(lambda: tsb.marginals(pot, out=out), warmup=1, iters=3)
+    rows.append({"config": "cfg4 shape (log)", "op": "marginals", "ms": ms,
+                 "tokens_per_s": cfg.B * cfg.N / (ms / 1e3), "kernel": tsb.last_kernel(),
+                 "hbm_frac": 2 * cfg.B * cfg.E * cfg.C * cfg.C * 4 / (ms / 1e3) / 6550e9})
     for r in rows:
         print(json.dumps(r), flush=True)
 
