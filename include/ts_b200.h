@@ -305,6 +305,12 @@ TS_API void ts_set_small_cluster(int G);
  * 0 = the general single-CTA kernel.  Results agree within the parity tolerances. */
 TS_API void ts_set_tiny(int enable);
 
+/* Debug/testing knob (process-global): 1 (default) streams the tiles of the wide-label log
+ * path (128 < C <= 256, C % 4 == 0) through a bulk-copy SMEM ring; 0 = plain coalesced
+ * loads into registers (the path odd widths always take).  Results agree within the
+ * parity tolerances. */
+TS_API void ts_set_wide_ring(int enable);
+
 /* Debug/testing knob (process-global): 1 (default) runs ts_marginals for C = 64 with one
  * serial chunk per sequence as the meet-in-the-middle kernel (forward and backward
  * recursions concurrently from both ends, marginals fused); 0 = separate forward and

@@ -469,6 +469,11 @@ def set_tiny(enable: bool) -> None:
     _lib.load().ts_set_tiny(1 if enable else 0)
 
 
+def set_wide_ring(enable: bool) -> None:
+    """Debug knob: bulk-copy SMEM ring for the wide-label (128 < C <= 256) log path."""
+    _lib.load().ts_set_wide_ring(1 if enable else 0)
+
+
 def set_meet(enable: bool) -> None:
     """Debug knob: meet-in-the-middle fused marginals kernel for C = 64 (default on)."""
     _lib.load().ts_set_meet(1 if enable else 0)

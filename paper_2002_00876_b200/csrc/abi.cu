@@ -1241,6 +1241,7 @@ TS_API void ts_set_small_cluster(int G) {
   g_small_cluster.store((G == 2 || G == 4) ? G : 0);
 }
 TS_API void ts_set_tiny(int enable) { g_tiny.store(enable ? 1 : 0); }
+TS_API void ts_set_wide_ring(int enable) { g_wide_ring = enable ? 1 : 0; }
 TS_API int ts_last_launch_count(void) { return t_launches; }
 TS_API const char* ts_last_kernel(void) { return t_kernel; }
 

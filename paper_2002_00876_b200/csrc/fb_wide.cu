@@ -4,7 +4,7 @@
 // Pass 1, grid (B, 2): CTA (b, 0) runs the forward recursion, CTA (b, 1) the backward one,
 // concurrently, each with 1024 threads and the exact per-cell max of §6(c):
 //   alpha_{t+1}[j] = LSE_i alpha_t[i] + l_t[i][j]        beta_t[i] = LSE_j l_t[i][j] + beta_{t+1}[j]
-// evaluated in log2 units as an online (max, sum) per output cell over batches of 16 terms
+// evaluated in log2 units as an online (max, sum) per output cell over batches of 8 terms
 // (one ex2 per term plus one per batch), so no range gate is needed.  Node vectors are
 // stored normalised (max 0) with fp64 offsets.  Forward: thread (j, q) reduces column j over
 // rows i = q (mod 4) (loads coalesced along j), four partials combined through SMEM.
@@ -14,7 +14,11 @@
 // Pass 2, one CTA per edge over the whole machine (marginals only):
 //   mu_t[i][j] = 2^(alpha_hat_t[i] + l_t[i][j] log2 e + beta_hat_{t+1}[j] + O^a_t + O^b_{t+1} - A log2 e)
 // (P:181-183), 0 beyond the sequence and for flagged sequences.
+// Pass 1 streams the tiles through a bulk-copy SMEM ring when C % 4 == 0
+// (fb_wide_ring_kernel, below) and with coalesced register loads otherwise.
 // Traffic: 2 reads of l in pass 1 (one per direction) + 1 read and 1 write in pass 2.
+// Measured at B64 N1024 C256 (ncu, profiles/r1e_wide_launches.csv): pass 1 9.6 ms (2 reads,
+// 55 % of HBM with 128 of 148 SMs streaming), pass 2 5.2 ms (1 read + 1 write at ~6.6 TB/s).
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -23,18 +27,19 @@ namespace tsb {
 namespace {
 constexpr int kWideThreads = 1024;
 constexpr int kWideMaxC = 256;
-constexpr int kBatch = 16;
+constexpr int kBatch = 8;
 
-// (m, s) <- (m, s) (+) batch of terms x[0..n) (log2 domain), online
+// (m, s) <- (m, s) (+) batch of NB terms x[] (log2 domain), online: NB + 1 ex2
+template <int NB = kBatch>
 __device__ __forceinline__ void online_add(float& m, float& s, const float* x) {
   float bm = x[0];
 #pragma unroll
-  for (int k = 1; k < kBatch; ++k) bm = fmaxf(bm, x[k]);
+  for (int k = 1; k < NB; ++k) bm = fmaxf(bm, x[k]);
   if (bm == neg_inf()) return;
   const float mn = fmaxf(m, bm);
   float acc = (m == neg_inf()) ? 0.f : s * ex2(m - mn);
 #pragma unroll
-  for (int k = 0; k < kBatch; ++k) acc += ex2(x[k] - mn);
+  for (int k = 0; k < NB; ++k) acc += ex2(x[k] - mn);
   m = mn;
   s = acc;
 }
@@ -102,7 +107,7 @@ __global__ void __launch_bounds__(kWideThreads, 1) fb_wide_sweep_kernel(SemiArgs
             bad |= (lv != lv) | (lv == pos_inf());
             x[k] = (i < C) ? fmaf(lv, kLog2e, v[i]) : neg_inf();
           }
-          online_add(m, sum, x);
+          online_add<kBatch>(m, sum, x);
         }
       }
       pm[q][j] = m;
@@ -133,16 +138,12 @@ __global__ void __launch_bounds__(kWideThreads, 1) fb_wide_sweep_kernel(SemiArgs
           float m = x[h][0];
 #pragma unroll
           for (int k = 1; k < KJ; ++k) m = fmaxf(m, x[h][k]);
+          m = warp_max(m);
           float sum = 0.f;
           if (m != neg_inf())
 #pragma unroll
             for (int k = 0; k < KJ; ++k) sum += ex2(x[h][k] - m);
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) {
-            const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
-            const float s2 = __shfl_xor_sync(0xffffffffu, sum, o);
-            lse_merge(m, sum, m2, s2);
-          }
+          sum = warp_sum(sum);
           const int i = i0 + 32 * h;
           if (lane == 0 && i < C) pm[0][i] = (m == neg_inf()) ? neg_inf() : m + lg2(sum);
         }
@@ -259,8 +260,201 @@ __global__ void __launch_bounds__(256) fb_wide_marg_kernel(SemiArgs a) {
   }
 }
 
+// ---- TMA-ring variant (C % 4 == 0: every 32-row block of a tile is 16-byte aligned) -------
+// Thread 0 streams each tile as ceil(C/32) contiguous 32-row blocks (1-D bulk copies, up to
+// 32 KB) into a kWideRing-slot SMEM ring, running up to kWideRing-1 blocks (across steps)
+// ahead of the consumers, so ~160 KB of l is in flight per SM independently of registers.
+// Forward: thread (j, q) takes rows q, q+4, ... of each block (8 terms, online LSE);
+// backward: warp w takes row w of each block (lanes along j).  Each warp releases a slot
+// with one arrival on its `empty` barrier (count 32).
+constexpr int kWideRing = 6;
+
+__device__ __forceinline__ void wide_issue(const SemiArgs& a, int64_t b, bool fwd, int64_t Eb,
+                                           int nblk, int64_t h, float* ring, uint64_t* full,
+                                           uint64_t* empty) {
+  const int C = (int)a.C;
+  const int64_t sh = h / nblk + 1;  // step of block h
+  if (sh > Eb) return;
+  const int kb = (int)(h - (sh - 1) * nblk);
+  const int64_t p = fwd ? sh : Eb - sh;
+  const int64_t t = fwd ? p - 1 : p;
+  const int slot = (int)(h % kWideRing);
+  if (h >= kWideRing) mbar_wait(&empty[slot], (uint32_t)(((h / kWideRing) - 1) & 1));
+  const int r0 = kb * 32, rows = (C - r0 < 32) ? C - r0 : 32;
+  const float* src = a.pot + ((b * (a.N - 1) + t) * C + r0) * (int64_t)C;
+  bulk_load(ring + (size_t)slot * 32 * C, src, (uint32_t)(rows * C * 4), &full[slot]);
+}
+
+__global__ void __launch_bounds__(kWideThreads, 1) fb_wide_ring_kernel(SemiArgs a) {
+  extern __shared__ __align__(128) float wring[];
+  __shared__ float vec[2][kWideMaxC];
+  __shared__ float pm[4][kWideMaxC], ps[4][kWideMaxC];
+  __shared__ float red[32];
+  __shared__ unsigned sbad;
+  __shared__ __align__(8) uint64_t full[kWideRing], empty[kWideRing];
+  const int C = (int)a.C;
+  const int64_t N = a.N;
+  const int64_t b = blockIdx.x;
+  const bool fwd = blockIdx.y == 0;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int64_t len = seq_len(a.lengths, b, N);
+  if (len < 0) {
+    if (fwd && tid == 0) {
+      a.logz[b] = qnan();
+      a.zbuf[b] = (double)qnan();
+      if (a.flags) a.flags[b] = TS_F_BADLEN;
+    }
+    return;
+  }
+  const int64_t Eb = len - 1;
+  const int nblk = (C + 31) / 32;
+  float* vh = (fwd ? a.ah : a.bh) + b * N * C;
+  double* vo = (fwd ? a.ao : a.bo) + b * N;
+  const int64_t n0 = fwd ? 0 : Eb;
+  if (tid < C) {
+    vec[0][tid] = 0.f;
+    vh[n0 * C + tid] = 0.f;
+  }
+  if (tid == 0) {
+    sbad = 0u;
+    vo[n0] = 0.0;
+    for (int k = 0; k < kWideRing; ++k) {
+      mbar_init(&full[k], 1);
+      mbar_init(&empty[k], 32);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int64_t h = 0; h < kWideRing - 1; ++h) wide_issue(a, b, fwd, Eb, nblk, h, wring, full, empty);
+  bool bad = false;
+  double off = 0.0;
+  bool dead = false;
+  int64_t g = 0;  // blocks consumed so far
+  for (int64_t s = 1; s <= Eb; ++s) {
+    const int64_t p = fwd ? s : Eb - s;
+    const float* v = vec[(s - 1) & 1];
+    float* vn = vec[s & 1];
+    float val = neg_inf();
+    const int j = tid & (kWideMaxC - 1), q = tid >> 8;
+    float m = neg_inf(), sum = 0.f;
+    for (int kb = 0; kb < nblk; ++kb, ++g) {
+      if (tid == 0) wide_issue(a, b, fwd, Eb, nblk, g + kWideRing - 1, wring, full, empty);
+      const int slot = (int)(g % kWideRing);
+      mbar_wait(&full[slot], (uint32_t)((g / kWideRing) & 1));
+      const float* blk = wring + (size_t)slot * 32 * C;
+      const int r0 = kb * 32;
+      if (fwd) {
+        if (j < C) {
+          float x[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const int r = q + 4 * k, i = r0 + r;
+            const float lv = (i < C) ? blk[r * C + j] : neg_inf();
+            bad |= (lv != lv) | (lv == pos_inf());
+            x[k] = (i < C) ? fmaf(lv, kLog2e, v[i]) : neg_inf();
+          }
+          online_add<8>(m, sum, x);
+        }
+      } else {
+        const int i = r0 + w;
+        if (i < C) {
+          float x[kWideMaxC / 32];
+          float mm = neg_inf();
+#pragma unroll
+          for (int k = 0; k < kWideMaxC / 32; ++k) {
+            const int jj = lane + 32 * k;
+            x[k] = (jj < C) ? fmaf(blk[w * C + jj], kLog2e, v[jj]) : neg_inf();
+            mm = fmaxf(mm, x[k]);
+          }
+          mm = warp_max(mm);  // row max first: one ex2 per term, no online merges
+          float ss = 0.f;
+          if (mm != neg_inf())
+#pragma unroll
+            for (int k = 0; k < kWideMaxC / 32; ++k) ss += ex2(x[k] - mm);
+          ss = warp_sum(ss);
+          if (lane == 0) pm[0][i] = (mm == neg_inf()) ? neg_inf() : mm + lg2(ss);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);
+    }
+    if (fwd) {
+      pm[q][j] = m;
+      ps[q][j] = sum;
+    }
+    __syncthreads();
+    if (tid < C) {
+      if (fwd) {
+        float M = pm[0][tid], S = ps[0][tid];
+#pragma unroll
+        for (int k = 1; k < 4; ++k) lse_merge(M, S, pm[k][tid], ps[k][tid]);
+        val = (M == neg_inf()) ? neg_inf() : M + lg2(S);
+      } else {
+        val = pm[0][tid];
+      }
+    }
+    if (tid < kWideMaxC) {
+      const float wm = warp_max(val);
+      if (lane == 0) red[w] = wm;
+    }
+    __syncthreads();
+    float Mx = red[0];
+#pragma unroll
+    for (int k = 1; k < kWideMaxC / 32; ++k) Mx = fmaxf(Mx, red[k]);
+    dead = dead || (Mx == neg_inf());
+    if (tid < C) {
+      const float nv = dead ? neg_inf() : val - Mx;
+      vn[tid] = nv;
+      vh[p * C + tid] = nv;
+    }
+    if (!dead) off += (double)Mx;
+    if (tid == 0) vo[p] = dead ? -INFINITY : off;
+    __syncthreads();
+  }
+  if (!fwd) return;
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&sbad, 1u);
+  __syncthreads();
+  if (tid < 32) {
+    const float* vE = vec[Eb & 1];
+    float sum = 0.f;
+    for (int jj = tid; jj < C; jj += 32) sum += ex2(vE[jj]);
+    sum = warp_sum(sum);
+    if (tid == 0) {
+      unsigned fl = 0;
+      double A;
+      if (sbad) {
+        fl = TS_F_NONFINITE;
+        A = (double)qnan();
+      } else if (dead) {
+        fl = TS_F_EMPTY;
+        A = -INFINITY;
+      } else {
+        A = kLn2 * (off + (double)lg2(sum));
+      }
+      a.zbuf[b] = A;
+      a.logz[b] = (float)A;
+      if (a.flags) a.flags[b] = fl;
+    }
+  }
+}
+
+int g_wide_ring = 1;  // debug knob (tests): 0 forces the register-path sweep
+
 cudaError_t launch_fb_wide(const SemiArgs& a, cudaStream_t st) {
-  fb_wide_sweep_kernel<<<dim3((unsigned)a.B, a.marg ? 2u : 1u), kWideThreads, 0, st>>>(a);
+  const dim3 grid((unsigned)a.B, a.marg ? 2u : 1u);
+  if (a.C % 4 == 0 && g_wide_ring) {
+    const size_t smem = (size_t)kWideRing * 32 * a.C * sizeof(float);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(fb_wide_ring_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)((size_t)kWideRing * 32 * kWideMaxC * sizeof(float)));
+      attr = true;
+    }
+    fb_wide_ring_kernel<<<grid, kWideThreads, smem, st>>>(a);
+  } else {
+    fb_wide_sweep_kernel<<<grid, kWideThreads, 0, st>>>(a);
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || !a.marg || a.N < 2) return e;
   fb_wide_marg_kernel<<<(unsigned)(a.B * (a.N - 1)), 256, 0, st>>>(a);

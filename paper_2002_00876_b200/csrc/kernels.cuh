@@ -193,6 +193,7 @@ struct SemiArgs {
 cudaError_t launch_semimarkov(const SemiArgs& a, cudaStream_t st);
 // linear chain, 128 < C <= 256 (fb_wide.cu): the SemiArgs workspace of K = 1
 cudaError_t launch_fb_wide(const SemiArgs& a, cudaStream_t st);
+extern int g_wide_ring;  // debug knob: 1 = SMEM ring (C % 4 == 0), 0 = register path
 // semi-Markov Viterbi (reading R18): seg [B][N] int32 out, score [B] out, bp [B][N][C] uint16
 // workspace ((k-1) * C + c'), flags as the other entry points
 struct SemiVitArgs {

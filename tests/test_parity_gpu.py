@@ -129,6 +129,19 @@ def test_log_wide_labels_masks_flags_ranges(dev, C):
     assert_log_parity(tsgen.wide_potentials(2, 30, C, seed=C, scale=50.0), None, dev)
 
 
+@pytest.mark.parametrize("C", [132, 200, 256])
+def test_log_wide_ring_matches_register_path(dev, C):
+    """The two wide-label sweeps (SMEM ring / registers) both match the oracle."""
+    pot = tsgen.potentials(3, 50, C, seed=31 + C)
+    lengths = np.array([50, 17, 1], np.int32)
+    try:
+        for ring in (True, False):
+            tsb.set_wide_ring(ring)
+            assert_log_parity(pot, lengths, dev)
+    finally:
+        tsb.set_wide_ring(True)
+
+
 def test_log_wide_cfg4_shape_full(dev):
     """logZ + marginals at cfg4's full shape (B64 N1024 C256, the log semiring) through
     fb_wide; oracle on sampled sequences (first, last) element by element, every sequence's
