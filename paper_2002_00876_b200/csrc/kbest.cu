@@ -8,12 +8,23 @@
 // >= K (keeping more candidates than K never changes the top K).  fp32 sums of dyadic
 // inputs are exact, so the result equals the fp64 oracle bit for bit.
 //
-// One CTA per sequence, thread j owns column j and keeps its sorted list in registers;
-// lists live in SMEM between steps; backpointers (i | r << 8) as uint16 [B][E][C][KM].
+// One CTA per sequence; column j is owned by a group of S consecutive lanes (S = 8, 4, 2, 1
+// as C allows <= 256 threads): lane s of the group inserts the candidates of labels
+// i = s (mod S) into a sorted register list, then the S partial lists are merged with KM
+// rounds of a shuffle arg-max over the group heads under the same (score desc, i asc,
+// r asc) key (the partial lists cover disjoint label sets, so the merge is exact).  Lists
+// live in SMEM between steps; backpointers (i | r << 8) as uint16 [B][E][C][KM].
 #include "common.cuh"
 #include "kernels.cuh"
 
 namespace tsb {
+
+// lanes per column: the largest power of two <= 8 with C * S <= 256
+__host__ __device__ inline int kbest_split(int C) {
+  int S = 8;
+  while (S > 1 && C * S > 256) S >>= 1;
+  return S;
+}
 
 template <int KM>
 __global__ void __launch_bounds__(256) kbest_kernel(KbestArgs a) {
@@ -22,7 +33,10 @@ __global__ void __launch_bounds__(256) kbest_kernel(KbestArgs a) {
   const int64_t N = a.N, E = N - 1, CC = (int64_t)C * C;
   const int64_t b = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, NW = blockDim.x >> 5;
-  const bool act = tid < C;
+  const bool act = tid < C;                        // final merge: thread = column
+  const int S = kbest_split(C);
+  const int jcol = tid / S, sidx = tid - jcol * S;  // step loop: S lanes per column
+  const bool actc = jcol < C;
   float* dl = ksm;                                  // [2][C][KM]
   float* rs = dl + 2 * (size_t)C * KM;              // [NW] block-reduction scores
   int* ri = reinterpret_cast<int*>(rs + NW);        // [NW] block-reduction labels
@@ -57,16 +71,17 @@ __global__ void __launch_bounds__(256) kbest_kernel(KbestArgs a) {
       rr[r] = 0;
     }
     const float* d = dl + (size_t)cur * C * KM;
-    if (act) {
-      const float* col = a.pot + (b * E + t) * CC + tid;
+    if (actc) {
+      const float* col = a.pot + (b * E + t) * CC + jcol;
       constexpr int kPf = 16;  // column values loaded per batch (independent loads in flight)
-      for (int i0 = 0; i0 < C; i0 += kPf) {
+      for (int i0 = sidx; i0 < C; i0 += S * kPf) {
         float lvs[kPf];
 #pragma unroll
-        for (int u = 0; u < kPf; ++u) lvs[u] = (i0 + u < C) ? col[(int64_t)(i0 + u) * C] : neg_inf();
+        for (int u = 0; u < kPf; ++u)
+          lvs[u] = (i0 + S * u < C) ? col[(int64_t)(i0 + S * u) * C] : neg_inf();
 #pragma unroll 1
-        for (int u = 0; u < kPf && i0 + u < C; ++u) {
-        const int i = i0 + u;
+        for (int u = 0; u < kPf && i0 + S * u < C; ++u) {
+        const int i = i0 + S * u;
         const float lv = lvs[u];
         nonfin |= (lv != lv) | (lv == pos_inf());
         if (lv == neg_inf()) continue;
@@ -93,12 +108,42 @@ __global__ void __launch_bounds__(256) kbest_kernel(KbestArgs a) {
         }
         }
       }
-      float* dn = dl + (size_t)(cur ^ 1) * C * KM + (size_t)tid * KM;
-      uint16_t* bpo = a.bp + ((b * E + t) * C + tid) * KM;
+    }
+    // merge the S partial lists of the group: KM rounds of a (score desc, i asc, r asc)
+    // arg-max over the group heads (every lane of the warp takes part in the shuffles)
+    {
+      float* dn = dl + (size_t)(cur ^ 1) * C * KM + (size_t)jcol * KM;
+      uint16_t* bpo = a.bp + ((b * E + t) * C + jcol) * KM;
+      int h = 0;
 #pragma unroll
-      for (int r = 0; r < KM; ++r) {
-        dn[r] = sc[r];
-        bpo[r] = (uint16_t)(ii[r] | (rr[r] << 8));
+      for (int out = 0; out < KM; ++out) {
+        float hv = neg_inf();
+        int hi = 0, hr = 0;
+#pragma unroll
+        for (int q = 0; q < KM; ++q)
+          if (q == h) {
+            hv = sc[q];
+            hi = ii[q];
+            hr = rr[q];
+          }
+        int src = sidx;
+        for (int o = 1; o < S; o <<= 1) {
+          const float ov = __shfl_xor_sync(0xffffffffu, hv, o);
+          const int oi = __shfl_xor_sync(0xffffffffu, hi, o);
+          const int orr = __shfl_xor_sync(0xffffffffu, hr, o);
+          const int os = __shfl_xor_sync(0xffffffffu, src, o);
+          if (ov > hv || (ov == hv && (oi < hi || (oi == hi && (orr < hr || (orr == hr && os < src)))))) {
+            hv = ov;
+            hi = oi;
+            hr = orr;
+            src = os;
+          }
+        }
+        if (src == sidx) ++h;
+        if (sidx == 0 && actc) {
+          dn[out] = hv;
+          bpo[out] = (uint16_t)(hi | (hr << 8));
+        }
       }
     }
     cur ^= 1;
@@ -188,7 +233,7 @@ size_t kbest_smem(int64_t C, int64_t K) {
 
 cudaError_t launch_kbest(const KbestArgs& a, cudaStream_t st) {
   const int km = kbest_km(a.K);
-  const int NT = (int)(((a.C + 31) / 32) * 32);
+  const int NT = (int)(((a.C * kbest_split((int)a.C) + 31) / 32) * 32);
   const size_t smem = kbest_smem(a.C, a.K);
   switch (km) {
     case 1: kbest_kernel<1><<<(unsigned)a.B, NT, smem, st>>>(a); break;
