@@ -22,6 +22,7 @@ for (B, N, C) in [(3, 25, 20), (2, 9, 3), (2, 70, 64), (2, 40, 128), (2, 300, 20
     tsb.viterbi(pot, lengths)
     tsb.marginals(pot, semiring="max")
     tsb.entropy(pot)
+    tsb.expectation(pot, pot)
     tsb.log_prob(pot, torch.zeros((B, N), dtype=torch.int32, device=dev))
     if C <= 128:
         tsb.sample(pot, torch.rand((2, B, N), device=dev))
@@ -39,6 +40,14 @@ sm = np.random.default_rng(0).standard_normal((2, 14, 3, 20, 20)).astype(np.floa
 tsb.semimarkov(T(sm))
 sm = np.random.default_rng(0).standard_normal((2, 14, 3, 100, 100)).astype(np.float32)
 tsb.semimarkov(T(sm))
+tsb.semimarkov_viterbi(T(sm))
+sm = np.random.default_rng(0).standard_normal((2, 14, 3, 20, 20)).astype(np.float32)
+tsb.semimarkov_viterbi(T(sm))
+# wide labels (fb_wide: SMEM ring for C % 4 == 0, register path otherwise)
+for Cw in (132, 131):
+    pw = T(tsgen.potentials(2, 30, Cw, seed=Cw))
+    tsb.marginals(pw, T(np.array([30, 9], np.int32)))
+    tsb.logpartition(pw)
 # time-sharded segments on one device
 from paper_2002_00876_b200 import dist as tdist  # noqa: E402
 pot = tsgen.potentials(2, 121, 20, seed=5)
