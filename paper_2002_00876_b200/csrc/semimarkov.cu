@@ -4,7 +4,9 @@
 // steps n -> n+k with label c2 after label c1 at node n; K = 1 is the linear chain).
 //
 // Segmental forward-backward, one CTA per sequence: the first GS threads (GS = 128 or 256
-// >= C) run the forward recursion (thread c), the next GS the backward one concurrently:
+// >= C) run the forward recursion, the next GS the backward one concurrently; within a
+// group S = 8/4/2/1 lanes share a label (C * S <= GS), each taking every S-th candidate
+// (k, c') as an online (max, sum) over batches of 8 loads, merged by shuffles:
 //   alpha_p[c] = LSE_{k <= min(K,p), c'} alpha_{p-k}[c'] + l[p-k, k-1, c', c]
 //   beta_p[c]  = LSE_{k <= min(K,E-p), c'} l[p, k-1, c, c'] + beta_{p+k}[c']
 // with the per-cell max of §6(c) and node vectors stored normalised (max 0) with
@@ -30,9 +32,16 @@ __device__ __forceinline__ float group_max(float v, float* red, int gw, int bar_
 }
 }  // namespace
 
+// lanes per label: the largest power of two <= 8 with C * S <= GS
+__device__ __forceinline__ int semi_split(int C, int GS) {
+  int S = 8;
+  while (S > 1 && C * S > GS) S >>= 1;
+  return S;
+}
+
 // GS = threads per recursion group: 128 (C <= 128) or 256 (C <= 256)
 template <int GS>
-__global__ void __launch_bounds__(2 * GS) semimarkov_kernel(SemiArgs a) {
+__global__ void __launch_bounds__(2 * GS, 1) semimarkov_kernel(SemiArgs a) {
   constexpr int kSmG = GS;
   extern __shared__ __align__(16) float ssm[];
   const int C = (int)a.C, K = (int)a.K;
@@ -45,6 +54,7 @@ __global__ void __launch_bounds__(2 * GS) semimarkov_kernel(SemiArgs a) {
   float* red0 = reinterpret_cast<float*>(reinterpret_cast<double*>(ssm + 2 * R * kSmG) + 2 * R);
   float* red = red0 + grp * 8;                           // [2][8] per-group reductions
   unsigned* sflag = reinterpret_cast<unsigned*>(red0 + 16);  // one word for the CTA
+  float* stage = reinterpret_cast<float*>(sflag + 4);         // [2][GS] label values
   const float* pb = a.pot + b * E * KCC;
   float* mg = a.marg ? a.marg + b * E * KCC : nullptr;
   const int64_t len = seq_len(a.lengths, b, N);
@@ -75,39 +85,64 @@ __global__ void __launch_bounds__(2 * GS) semimarkov_kernel(SemiArgs a) {
     }
   }
   named_bar(1 + grp, kSmG);
+  // S lanes per label: lane sl of label cl takes the candidates f = (k-1) C + c' with
+  // f = sl (mod S), an online (max, sum) over batches of 8 loads, merged by shuffles
+  const int S = semi_split(C, kSmG);
+  const int cl = c / S, sl = c - cl * S;
+  const bool actl = cl < C;
   for (int64_t s = 1; s <= Eb; ++s) {
     const int64_t p = grp == 0 ? s : Eb - s;             // node computed at this step
     const int64_t pr = grp == 0 ? p - 1 : p + 1;         // reference node (offset frame)
     const int kmax = (int)(grp == 0 ? (p < K ? p : K) : (Eb - p < K ? Eb - p : K));
     const double oref = ooff[pr % R];
-    float m = neg_inf();
-    for (int k = 1; k <= kmax; ++k) {
-      const int64_t q = grp == 0 ? p - k : p + k;        // the other end of the segment
-      const float d = (float)(ooff[q % R] - oref);
-      const float* vq = ring + (q % R) * kSmG;
-      const float* lt = grp == 0 ? pb + (p - k) * KCC + (int64_t)(k - 1) * C * C
-                                 : pb + p * KCC + (int64_t)(k - 1) * C * C;
-      if (act)
-        for (int c2 = 0; c2 < C; ++c2) {
-          const float lv = grp == 0 ? lt[(int64_t)c2 * C + c] : lt[(int64_t)c * C + c2];
-          bad |= (lv != lv) | (lv == pos_inf());
-          m = fmaxf(m, d + vq[c2] + lv);
+    float m = neg_inf(), sum = 0.f;
+    if (actl) {
+      const int nf = kmax * C;
+      for (int f0 = sl; f0 < nf; f0 += 8 * S) {
+        float x[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int f = f0 + u * S;
+          float xv = neg_inf();
+          if (f < nf) {
+            const int k = f / C + 1, c2 = f - (k - 1) * C;
+            const int64_t q = grp == 0 ? p - k : p + k;    // the other end of the segment
+            const float* lt = grp == 0 ? pb + (p - k) * KCC + (int64_t)(k - 1) * C * C
+                                       : pb + p * KCC + (int64_t)(k - 1) * C * C;
+            const float lv = grp == 0 ? lt[(int64_t)c2 * C + cl] : lt[(int64_t)cl * C + c2];
+            bad |= (lv != lv) | (lv == pos_inf());
+            xv = ((float)(ooff[q % R] - oref) + ring[(q % R) * kSmG + c2] + lv) * kLog2e;
+          }
+          x[u] = xv;
         }
-    }
-    float sum = 0.f;
-    if (act && m != neg_inf())
-      for (int k = 1; k <= kmax; ++k) {
-        const int64_t q = grp == 0 ? p - k : p + k;
-        const float d = (float)(ooff[q % R] - oref);
-        const float* vq = ring + (q % R) * kSmG;
-        const float* lt = grp == 0 ? pb + (p - k) * KCC + (int64_t)(k - 1) * C * C
-                                   : pb + p * KCC + (int64_t)(k - 1) * C * C;
-        for (int c2 = 0; c2 < C; ++c2) {
-          const float lv = grp == 0 ? lt[(int64_t)c2 * C + c] : lt[(int64_t)c * C + c2];
-          sum += ex2((d + vq[c2] + lv - m) * kLog2e);
+        float bm = x[0];
+#pragma unroll
+        for (int u = 1; u < 8; ++u) bm = fmaxf(bm, x[u]);
+        if (bm != neg_inf()) {
+          const float mn = fmaxf(m, bm);
+          float acc = (m == neg_inf()) ? 0.f : sum * ex2(m - mn);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) acc += ex2(x[u] - mn);
+          m = mn;
+          sum = acc;
         }
       }
-    const float val = (act && m != neg_inf()) ? m + lg2(sum) * (float)kLn2 : neg_inf();
+    }
+    for (int o = 1; o < S; o <<= 1) {  // merge the S partial (max, sum) pairs (log2 units)
+      const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
+      const float s2 = __shfl_xor_sync(0xffffffffu, sum, o);
+      const float M2 = fmaxf(m, m2);
+      if (M2 != neg_inf()) {
+        sum = ((m == neg_inf()) ? 0.f : sum * ex2(m - M2)) + ((m2 == neg_inf()) ? 0.f : s2 * ex2(m2 - M2));
+        m = M2;
+      }
+    }
+    // the label's value, moved to thread c = label (the layout of the ring and vh)
+    const float lval = (m == neg_inf()) ? neg_inf() : (m + lg2(sum)) * (float)kLn2;
+    if (actl && sl == 0) stage[grp * kSmG + cl] = lval;
+    named_bar(1 + grp, kSmG);
+    const bool act2 = c < C;
+    const float val = act2 ? stage[grp * kSmG + c] : neg_inf();
     const float M = group_max<GS>(val, red, gw, 1 + grp);
     const bool dead = (M == neg_inf());
     const float nv = (act && !dead) ? val - M : neg_inf();
@@ -178,7 +213,7 @@ cudaError_t launch_semimarkov(const SemiArgs& a, cudaStream_t st) {
   const int R = (int)a.K + 1;
   const int GS = a.C <= 128 ? 128 : 256;
   const size_t smem = (size_t)2 * R * GS * sizeof(float) + (size_t)2 * R * sizeof(double) +
-                      16 * sizeof(float) + 16;
+                      16 * sizeof(float) + 16 + (size_t)2 * GS * sizeof(float);
   if (GS == 128)
     semimarkov_kernel<128><<<(unsigned)a.B, 256, smem, st>>>(a);
   else
