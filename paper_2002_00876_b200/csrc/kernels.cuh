@@ -189,6 +189,7 @@ struct SemiArgs {
   double* ao;              // [B][N] natural offsets
   double* bo;
   double* zbuf;            // [B] logZ in fp64
+  int staged;              // semimarkov_kernel: tiles staged in SMEM one step ahead (launcher)
 };
 cudaError_t launch_semimarkov(const SemiArgs& a, cudaStream_t st);
 // linear chain, 128 < C <= 256 (fb_wide.cu): the SemiArgs workspace of K = 1
@@ -204,6 +205,7 @@ struct SemiVitArgs {
   float* score;
   uint32_t* flags;
   uint16_t* bp;
+  int staged;              // set by the launcher: tiles staged in SMEM one step ahead
 };
 cudaError_t launch_semimarkov_viterbi(const SemiVitArgs& a, cudaStream_t st);
 

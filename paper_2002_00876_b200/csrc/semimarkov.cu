@@ -6,7 +6,7 @@
 // Segmental forward-backward, one CTA per sequence: the first GS threads (GS = 128 or 256
 // >= C) run the forward recursion, the next GS the backward one concurrently; within a
 // group S = 8/4/2/1 lanes share a label (C * S <= GS), each taking every S-th candidate
-// (k, c') as an online (max, sum) over batches of 8 loads, merged by shuffles:
+// (k, c') as an online (max, sum) over chunks of 4 loads, merged by shuffles:
 //   alpha_p[c] = LSE_{k <= min(K,p), c'} alpha_{p-k}[c'] + l[p-k, k-1, c', c]
 //   beta_p[c]  = LSE_{k <= min(K,E-p), c'} l[p, k-1, c, c'] + beta_{p+k}[c']
 // with the per-cell max of §6(c) and node vectors stored normalised (max 0) with
@@ -55,6 +55,7 @@ __global__ void __launch_bounds__(2 * GS, 1) semimarkov_kernel(SemiArgs a) {
   float* red = red0 + grp * 8;                           // [2][8] per-group reductions
   unsigned* sflag = reinterpret_cast<unsigned*>(red0 + 16);  // one word for the CTA
   float* stage = reinterpret_cast<float*>(sflag + 4);         // [2][GS] label values
+  float* stg = stage + 2 * kSmG + grp * 2 * K * C * C;        // [2 grp][2][K][C][C] (a.staged)
   const float* pb = a.pot + b * E * KCC;
   float* mg = a.marg ? a.marg + b * E * KCC : nullptr;
   const int64_t len = seq_len(a.lengths, b, N);
@@ -84,9 +85,27 @@ __global__ void __launch_bounds__(2 * GS, 1) semimarkov_kernel(SemiArgs a) {
       vo[n0] = 0.0;
     }
   }
+  // staged: the tiles a step reads are copied to SMEM with cp.async one step ahead
+  // (forward node p: l[p-k][k-1]; backward node p: l[p][k-1], k <= K within the sequence)
+  const int64_t CC2 = (int64_t)C * C;
+  auto issue = [&](int64_t ss) {
+    const int64_t pp = grp == 0 ? ss : Eb - ss;
+    const int km = (int)(grp == 0 ? (pp < K ? pp : K) : (Eb - pp < K ? Eb - pp : K));
+    float* dst = stg + (ss & 1) * K * CC2;
+    for (int k = 1; k <= km; ++k) {
+      const float* src = grp == 0 ? pb + (pp - k) * KCC + (int64_t)(k - 1) * CC2
+                                  : pb + pp * KCC + (int64_t)(k - 1) * CC2;
+      for (int64_t r = c; r < CC2; r += kSmG) cp_async4(dst + (k - 1) * CC2 + r, src + r);
+    }
+    cp_async_commit();
+  };
+  if (a.staged && Eb >= 1) {
+    issue(1);
+    cp_async_wait<0>();
+  }
   named_bar(1 + grp, kSmG);
-  // S lanes per label: lane sl of label cl takes the candidates f = (k-1) C + c' with
-  // f = sl (mod S), an online (max, sum) over batches of 8 loads, merged by shuffles
+  // S lanes per label: lane sl of label cl takes the candidates (k, c') with c' = sl (mod S),
+  // an online (max, sum) over chunks of 4 loads, merged by shuffles
   const int S = semi_split(C, kSmG);
   const int cl = c / S, sl = c - cl * S;
   const bool actl = cl < C;
@@ -96,35 +115,43 @@ __global__ void __launch_bounds__(2 * GS, 1) semimarkov_kernel(SemiArgs a) {
     const int kmax = (int)(grp == 0 ? (p < K ? p : K) : (Eb - p < K ? Eb - p : K));
     const double oref = ooff[pr % R];
     float m = neg_inf(), sum = 0.f;
+    if (a.staged && s + 1 <= Eb) issue(s + 1);
     if (actl) {
-      const int nf = kmax * C;
-      for (int f0 = sl; f0 < nf; f0 += 8 * S) {
-        float x[8];
+      // per segment length k: the offset delta and the source rows are hoisted; lane sl
+      // takes c' = sl, sl + S, ... in chunks of 4 (online (max, sum), log2 units)
+      for (int k = 1; k <= kmax; ++k) {
+        const int64_t q = grp == 0 ? p - k : p + k;      // the other end of the segment
+        const int qs = (int)(q % R);
+        const float d = (float)(ooff[qs] - oref);
+        const float* vq = ring + qs * kSmG;
+        const float* lt = a.staged ? stg + (s & 1) * K * CC2 + (k - 1) * CC2
+                          : (grp == 0 ? pb + (p - k) * KCC + (int64_t)(k - 1) * CC2
+                                      : pb + p * KCC + (int64_t)(k - 1) * CC2);
+        // forward reads column cl (stride C), backward row cl (stride 1)
+        const float* lp = grp == 0 ? lt + cl : lt + (int64_t)cl * C;
+        const int ls = grp == 0 ? C : 1;
+        for (int c0 = sl; c0 < C; c0 += 4 * S) {
+          float x[4];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int f = f0 + u * S;
-          float xv = neg_inf();
-          if (f < nf) {
-            const int k = f / C + 1, c2 = f - (k - 1) * C;
-            const int64_t q = grp == 0 ? p - k : p + k;    // the other end of the segment
-            const float* lt = grp == 0 ? pb + (p - k) * KCC + (int64_t)(k - 1) * C * C
-                                       : pb + p * KCC + (int64_t)(k - 1) * C * C;
-            const float lv = grp == 0 ? lt[(int64_t)c2 * C + cl] : lt[(int64_t)cl * C + c2];
-            bad |= (lv != lv) | (lv == pos_inf());
-            xv = ((float)(ooff[q % R] - oref) + ring[(q % R) * kSmG + c2] + lv) * kLog2e;
+          for (int u = 0; u < 4; ++u) {
+            const int c2 = c0 + u * S;
+            float xv = neg_inf();
+            if (c2 < C) {
+              const float lv = lp[c2 * ls];
+              bad |= (lv != lv) | (lv == pos_inf());
+              xv = (d + vq[c2] + lv) * kLog2e;
+            }
+            x[u] = xv;
           }
-          x[u] = xv;
-        }
-        float bm = x[0];
+          const float bm = fmaxf(fmaxf(x[0], x[1]), fmaxf(x[2], x[3]));
+          if (bm != neg_inf()) {
+            const float mn = fmaxf(m, bm);
+            float acc = (m == neg_inf()) ? 0.f : sum * ex2(m - mn);
 #pragma unroll
-        for (int u = 1; u < 8; ++u) bm = fmaxf(bm, x[u]);
-        if (bm != neg_inf()) {
-          const float mn = fmaxf(m, bm);
-          float acc = (m == neg_inf()) ? 0.f : sum * ex2(m - mn);
-#pragma unroll
-          for (int u = 0; u < 8; ++u) acc += ex2(x[u] - mn);
-          m = mn;
-          sum = acc;
+            for (int u = 0; u < 4; ++u) acc += ex2(x[u] - mn);
+            m = mn;
+            sum = acc;
+          }
         }
       }
     }
@@ -153,6 +180,7 @@ __global__ void __launch_bounds__(2 * GS, 1) semimarkov_kernel(SemiArgs a) {
       ooff[p % R] = o;
       vo[p] = dead ? -INFINITY : o;
     }
+    if (a.staged) cp_async_wait<0>();
     named_bar(1 + grp, kSmG);
   }
   if (__any_sync(0xffffffffu, bad) && (tid & 31) == 0) atomicOr(sflag, (unsigned)TS_F_NONFINITE);
@@ -194,26 +222,52 @@ __global__ void __launch_bounds__(2 * GS, 1) semimarkov_kernel(SemiArgs a) {
   const float* bh = a.bh + b * N * C;
   const double* ao = a.ao + b * N;
   const double* bo = a.bo + b * N;
-  for (int64_t q = tid; q < E * KCC; q += blockDim.x) {
-    const int64_t n = q / KCC;
-    const int64_t rem = q - n * KCC;
-    const int k = (int)(rem / ((int64_t)C * C)) + 1;
-    const int c1 = (int)((rem / C) % C), c2 = (int)(rem % C);
-    float v = 0.f;
-    if (!fl && n + k <= Eb) {
-      const double off = ao[n] + bo[n + k] - A;
-      const float x = (float)off + ah[n * C + c1] + pb[q] + bh[(n + k) * C + c2];
-      v = (x == neg_inf() || !(off > -INFINITY)) ? 0.f : ex2(x * kLog2e);
+  // one (n, k) tile at a time: the offsets are per tile, element indices need no 64-bit
+  // division; warps take tiles round-robin, lanes stride the C x C elements
+  const int64_t CCt = (int64_t)C * C;
+  const int nw = blockDim.x >> 5, wid = tid >> 5, ln = tid & 31;
+  for (int64_t nk = wid; nk < E * K; nk += nw) {
+    const int64_t n = nk / K;
+    const int k = (int)(nk - n * K) + 1;
+    float* mq = mg + nk * CCt;
+    const bool live = !fl && n + k <= Eb;
+    const double offd = live ? ao[n] + bo[n + k] - A : 0.0;
+    const bool ok = live && offd > -INFINITY;
+    const float off = (float)offd;
+    const float* lq = pb + nk * CCt;
+    const float* ahn = ah + n * C;
+    const float* bhn = bh + (n + k) * C;
+    for (int r = ln; r < (int)CCt; r += 32) {
+      float v = 0.f;
+      if (ok) {
+        const int c1 = r / C, c2 = r - c1 * C;
+        const float x = off + ahn[c1] + lq[r] + bhn[c2];
+        v = (x == neg_inf()) ? 0.f : ex2(x * kLog2e);
+      }
+      mq[r] = v;
     }
-    mg[q] = v;
   }
 }
 
-cudaError_t launch_semimarkov(const SemiArgs& a, cudaStream_t st) {
+constexpr size_t kSemiStageBytes = 96 * 1024;  // staged tiles only when 4 K C^2 floats fit
+
+cudaError_t launch_semimarkov(const SemiArgs& a0, cudaStream_t st) {
+  SemiArgs a = a0;
   const int R = (int)a.K + 1;
   const int GS = a.C <= 128 ? 128 : 256;
+  const size_t stage_bytes = (size_t)4 * a.K * a.C * a.C * sizeof(float);
+  a.staged = stage_bytes <= kSemiStageBytes ? 1 : 0;
   const size_t smem = (size_t)2 * R * GS * sizeof(float) + (size_t)2 * R * sizeof(double) +
-                      16 * sizeof(float) + 16 + (size_t)2 * GS * sizeof(float);
+                      16 * sizeof(float) + 16 + (size_t)2 * GS * sizeof(float) +
+                      (a.staged ? stage_bytes : 0);
+  static bool attr = false;
+  if (!attr) {
+    const int mx = (int)((size_t)2 * 17 * 256 * sizeof(float) + 2 * 17 * sizeof(double) + 64 +
+                         2 * 256 * sizeof(float) + kSemiStageBytes);
+    cudaFuncSetAttribute(semimarkov_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(semimarkov_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    attr = true;
+  }
   if (GS == 128)
     semimarkov_kernel<128><<<(unsigned)a.B, 256, smem, st>>>(a);
   else
@@ -237,6 +291,7 @@ __global__ void __launch_bounds__(256) semimarkov_viterbi_kernel(SemiVitArgs a) 
   float* rv = ring + R * NT;                            // [8] block arg-max values
   int* ri = reinterpret_cast<int*>(rv + 8);             // [8] block arg-max labels
   unsigned* sflag = reinterpret_cast<unsigned*>(ri + 8);
+  float* stg = reinterpret_cast<float*>(sflag + 4);     // [2][K][C][C] staged tiles (a.staged)
   const float* pb = a.pot + b * E * KCC;
   int32_t* sg = a.seg + b * N;
   uint16_t* bp = a.bp + b * N * C;
@@ -250,38 +305,71 @@ __global__ void __launch_bounds__(256) semimarkov_viterbi_kernel(SemiVitArgs a) 
     return;
   }
   const int64_t Eb = len - 1;
-  const bool act = tid < C;
+  const bool act = tid < C;                             // final arg-max: thread = label
+  const int S = semi_split(C, 256);                     // step loop: S lanes per label
+  const int cl = tid / S, sl = tid - cl * S;
+  const bool actl = cl < C;
   if (tid == 0) *sflag = 0u;
   ring[tid] = act ? 0.f : neg_inf();                    // delta_0 = 0 (node 0 in slot 0)
+  // staged: the tiles node p reads (l[p-k][k-1], k <= min(K,p)) are copied to SMEM with
+  // cp.async one step ahead, so each step waits for one memory round trip, not one per batch
+  const int64_t CC2 = (int64_t)C * C;
+  auto issue = [&](int64_t pp) {
+    float* dst = stg + (pp & 1) * K * CC2;
+    const int km = (int)(pp < K ? pp : K);
+    for (int k = 1; k <= km; ++k) {
+      const float* src = pb + (pp - k) * KCC + (int64_t)(k - 1) * CC2;
+      for (int64_t r = tid; r < CC2; r += NT) cp_async4(dst + (k - 1) * CC2 + r, src + r);
+    }
+    cp_async_commit();
+  };
+  if (a.staged && Eb >= 1) {
+    issue(1);
+    cp_async_wait<0>();
+  }
   __syncthreads();
   bool bad = false;
   for (int64_t p = 1; p <= Eb; ++p) {
     float best = neg_inf();
     int arg = 0;
-    if (act) {
+    if (a.staged && p + 1 <= Eb) issue(p + 1);
+    if (actl) {
       const int kmax = (int)(p < K ? p : K);
       for (int k = 1; k <= kmax; ++k) {
-        const float* dq = ring + ((p - k) % R) * NT;
-        const float* col = pb + (p - k) * KCC + (int64_t)(k - 1) * C * C + tid;
-        constexpr int kPf = 8;  // column values loaded per batch (independent loads in flight)
-        for (int i0 = 0; i0 < C; i0 += kPf) {
-          float lv[kPf];
+        const float* dq = ring + (int)((p - k) % R) * NT;
+        const float* col = a.staged ? stg + (p & 1) * K * CC2 + (k - 1) * CC2 + cl
+                                    : pb + (p - k) * KCC + (int64_t)(k - 1) * CC2 + cl;
+        for (int i0 = sl; i0 < C; i0 += 4 * S) {
+          float lv[4];
 #pragma unroll
-          for (int u = 0; u < kPf; ++u) lv[u] = (i0 + u < C) ? col[(int64_t)(i0 + u) * C] : neg_inf();
+          for (int u = 0; u < 4; ++u) lv[u] = (i0 + u * S < C) ? col[(int64_t)(i0 + u * S) * C] : neg_inf();
 #pragma unroll
-          for (int u = 0; u < kPf; ++u) {
+          for (int u = 0; u < 4; ++u) {
+            const int i = i0 + u * S;
             bad |= (lv[u] != lv[u]) | (lv[u] == pos_inf());
-            const float v = dq[i0 + u < C ? i0 + u : 0] + lv[u];
+            const float v = dq[i < C ? i : 0] + lv[u];
             if (v > best) {
               best = v;
-              arg = (k - 1) * C + i0 + u;
+              arg = (k - 1) * C + i;
             }
           }
         }
       }
-      bp[p * C + tid] = (uint16_t)arg;
     }
-    ring[(p % R) * NT + tid] = act ? best : neg_inf();
+    // merge the S lanes of a label: max value, ties -> the smallest (k, c') (= serial order)
+    for (int o = 1; o < S; o <<= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oa = __shfl_xor_sync(0xffffffffu, arg, o);
+      if (ov > best || (ov == best && oa < arg)) {
+        best = ov;
+        arg = oa;
+      }
+    }
+    if (actl && sl == 0) {
+      bp[p * C + cl] = (uint16_t)arg;
+      ring[(p % R) * NT + cl] = best;
+    }
+    if (a.staged) cp_async_wait<0>();
     __syncthreads();
   }
   if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(sflag, 1u);
@@ -334,14 +422,32 @@ __global__ void __launch_bounds__(256) semimarkov_viterbi_kernel(SemiVitArgs a) 
   }
 }
 
-size_t semimarkov_viterbi_smem(int64_t C, int64_t K) {
-  const int NT = (int)(((C + 31) / 32) * 32);
-  return (size_t)(K + 1) * NT * sizeof(float) + 8 * sizeof(float) + 8 * sizeof(int) + 16;
+constexpr size_t kSemiStageMax = 96 * 1024;  // staged tiles only when 2 K C^2 floats fit
+
+int semimarkov_viterbi_threads(int64_t C) {
+  int S = 8;
+  while (S > 1 && C * S > 256) S >>= 1;
+  return (int)(((C * S + 31) / 32) * 32);
 }
 
-cudaError_t launch_semimarkov_viterbi(const SemiVitArgs& a, cudaStream_t st) {
-  const int NT = (int)(((a.C + 31) / 32) * 32);
-  semimarkov_viterbi_kernel<<<(unsigned)a.B, NT, semimarkov_viterbi_smem(a.C, a.K), st>>>(a);
+size_t semimarkov_viterbi_smem(int64_t C, int64_t K, bool staged) {
+  const int NT = semimarkov_viterbi_threads(C);
+  return (size_t)(K + 1) * NT * sizeof(float) + 8 * sizeof(float) + 8 * sizeof(int) + 16 +
+         (staged ? (size_t)2 * K * C * C * sizeof(float) : 0);
+}
+
+cudaError_t launch_semimarkov_viterbi(const SemiVitArgs& a0, cudaStream_t st) {
+  SemiVitArgs a = a0;
+  a.staged = (size_t)2 * a.K * a.C * a.C * sizeof(float) <= kSemiStageMax ? 1 : 0;
+  const int NT = semimarkov_viterbi_threads(a.C);
+  const size_t smem = semimarkov_viterbi_smem(a.C, a.K, a.staged != 0);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(semimarkov_viterbi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(semimarkov_viterbi_smem(256, 16, false) + kSemiStageMax));
+    attr = true;
+  }
+  semimarkov_viterbi_kernel<<<(unsigned)a.B, NT, smem, st>>>(a);
   return cudaGetLastError();
 }
 
