@@ -5,8 +5,11 @@
 //   bp_t[j] = the smallest i attaining the max (strict '>' while scanning i upward);
 //   z_E = smallest argmax_j delta_E[j];  z_t = bp_t[z_{t+1}];  score = delta_E[z_E].
 // fp32 adds of dyadic inputs are exact, so delta equals the fp64 oracle bit-for-bit.
-// One CTA per sequence, thread j owns column j; tiles stream through a cp.async ring of
-// row blocks (a 256 x 256 tile is 256 KB, larger than SMEM).
+// One CTA per sequence; column j is owned by SL = 8/4/2/1 consecutive lanes (C * SL <= 256),
+// lane s scanning rows i = s (mod SL) in two interleaved compare chains; the SL partial
+// (max, first index) pairs are merged by shuffles at the end of each tile (smaller index on
+// ties: reading R5).  Tiles stream through a cp.async ring of row blocks (a 256 x 256 tile
+// is 256 KB, larger than SMEM).
 #include <atomic>
 
 #include "common.cuh"
@@ -20,7 +23,13 @@ __device__ __forceinline__ float max_nan(float a, float b) {
   asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
   return r;
 }
-inline int vit_threads(int64_t C) { return (int)(((C + 31) / 32) * 32); }
+// lanes per column: the largest power of two <= 8 with C * SL <= 256
+inline int vit_lanes(int64_t C) {
+  int SL = 8;
+  while (SL > 1 && C * SL > 256) SL >>= 1;
+  return SL;
+}
+inline int vit_threads(int64_t C) { return (int)(((C * vit_lanes(C) + 31) / 32) * 32); }
 inline int vit_rows(int64_t C) { return C <= 128 ? (int)C : 32; }
 }  // namespace
 
@@ -58,7 +67,11 @@ __global__ void __launch_bounds__(256) viterbi_fwd_kernel(VitArgs a, int S, int 
   const int nblk = (C + RB - 1) / RB;
   const int64_t G = Eb * nblk;
   const float* potb = a.pot + b * E * CC;
-  const bool act = tid < C;
+  const bool act = tid < C;                       // label-indexed work (delta, final arg-max)
+  int SL = 8;
+  while (SL > 1 && C * SL > 256) SL >>= 1;
+  const int col = tid / SL, sl = tid - col * SL;  // the step loop: SL lanes per column
+  const bool actc = col < C;
 
   auto issue = [&](int64_t g) {
     if (g < G) {
@@ -91,16 +104,16 @@ __global__ void __launch_bounds__(256) viterbi_fwd_kernel(VitArgs a, int S, int 
     const int r0 = blk * RB, nr = min(RB, C - r0);
     const float* tile = ring + (size_t)(g % S) * SF;
     const float* d = dl + buf * NT + r0;
-    if (act) {
+    if (actc) {
       // two interleaved row streams (independent compare chains), merged with the
       // smallest-index rule on ties (reading R5)
       float best1 = neg_inf();
       int arg1 = 0x7fffffff;
-      int r = 0;
+      int r = sl;
 #pragma unroll 2
-      for (; r + 1 < nr; r += 2) {
-        const float v0 = d[r] + tile[r * C + tid];
-        const float v1 = d[r + 1] + tile[(r + 1) * C + tid];
+      for (; r + SL < nr; r += 2 * SL) {
+        const float v0 = d[r] + tile[r * C + col];
+        const float v1 = d[r + SL] + tile[(r + SL) * C + col];
         chk = max_nan(chk, max_nan(v0, v1));
         if (v0 > best) {
           best = v0;
@@ -108,11 +121,11 @@ __global__ void __launch_bounds__(256) viterbi_fwd_kernel(VitArgs a, int S, int 
         }
         if (v1 > best1) {
           best1 = v1;
-          arg1 = r0 + r + 1;
+          arg1 = r0 + r + SL;
         }
       }
       if (r < nr) {
-        const float v0 = d[r] + tile[r * C + tid];
+        const float v0 = d[r] + tile[r * C + col];
         chk = max_nan(chk, v0);
         if (v0 > best) {
           best = v0;
@@ -125,9 +138,20 @@ __global__ void __launch_bounds__(256) viterbi_fwd_kernel(VitArgs a, int S, int 
       }
     }
     if (blk == nblk - 1) {
+      for (int o = 1; o < SL; o <<= 1) {  // merge the SL lanes of the column
+        const float ov = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oa = __shfl_xor_sync(0xffffffffu, arg, o);
+        chk = max_nan(chk, __shfl_xor_sync(0xffffffffu, chk, o));
+        if (ov > best || (ov == best && oa < arg)) {
+          best = ov;
+          arg = oa;
+        }
+      }
       const float nd = (chk != chk) ? qnan() : best;
-      dl[(buf ^ 1) * NT + tid] = act ? nd : neg_inf();
-      if (act) a.bp[(b * E + t) * C + tid] = (uint8_t)arg;
+      if (actc && sl == 0) {
+        dl[(buf ^ 1) * NT + col] = nd;
+        a.bp[(b * E + t) * C + col] = (uint8_t)arg;
+      }
       best = neg_inf();
       chk = neg_inf();
       arg = 0;
