@@ -9,7 +9,7 @@
 // inputs are exact, so the result equals the fp64 oracle bit for bit.
 //
 // One CTA per sequence; column j is owned by a group of S consecutive lanes (S = 8, 4, 2, 1
-// as C allows <= 256 threads): lane s of the group inserts the candidates of labels
+// as C allows <= 512 threads): lane s of the group inserts the candidates of labels
 // i = s (mod S) into a sorted register list, then the S partial lists are merged with KM
 // rounds of a shuffle arg-max over the group heads under the same (score desc, i asc,
 // r asc) key (the partial lists cover disjoint label sets, so the merge is exact).  Lists
@@ -19,15 +19,15 @@
 
 namespace tsb {
 
-// lanes per column: the largest power of two <= 8 with C * S <= 256
+// lanes per column: the largest power of two <= 8 with C * S <= 512
 __host__ __device__ inline int kbest_split(int C) {
   int S = 8;
-  while (S > 1 && C * S > 256) S >>= 1;
+  while (S > 1 && C * S > 512) S >>= 1;
   return S;
 }
 
 template <int KM>
-__global__ void __launch_bounds__(256) kbest_kernel(KbestArgs a) {
+__global__ void __launch_bounds__(512) kbest_kernel(KbestArgs a) {
   extern __shared__ __align__(16) float ksm[];
   const int C = (int)a.C;
   const int64_t N = a.N, E = N - 1, CC = (int64_t)C * C;
@@ -228,7 +228,7 @@ int kbest_km(int64_t K) {
 
 size_t kbest_smem(int64_t C, int64_t K) {
   const int km = kbest_km(K);
-  return (2 * (size_t)C * km + 8) * sizeof(float) + 8 * sizeof(int) + 2 * (size_t)K * sizeof(int) + 16;
+  return (2 * (size_t)C * km + 16) * sizeof(float) + 16 * sizeof(int) + 2 * (size_t)K * sizeof(int) + 16;
 }
 
 cudaError_t launch_kbest(const KbestArgs& a, cudaStream_t st) {
