@@ -17,8 +17,9 @@
 // Pass 1 streams the tiles through a bulk-copy SMEM ring when C % 4 == 0
 // (fb_wide_ring_kernel, below) and with coalesced register loads otherwise.
 // Traffic: 2 reads of l in pass 1 (one per direction) + 1 read and 1 write in pass 2.
-// Measured at B64 N1024 C256 (ncu, profiles/r1e_wide_launches.csv): pass 1 9.6 ms (2 reads,
-// 55 % of HBM with 128 of 148 SMs streaming), pass 2 5.2 ms (1 read + 1 write at ~6.6 TB/s).
+// Measured at B64 N1024 C256: pass 1 8.5 ms (2 reads, 62 % of HBM with 128 of 148 SMs
+// streaming; 9.6 ms in profiles/r1e_wide_launches.csv, before the producer warp), pass 2
+// 5.2 ms (1 read + 1 write at ~6.6 TB/s).
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -261,12 +262,12 @@ __global__ void __launch_bounds__(256) fb_wide_marg_kernel(SemiArgs a) {
 }
 
 // ---- TMA-ring variant (C % 4 == 0: every 32-row block of a tile is 16-byte aligned) -------
-// Thread 0 streams each tile as ceil(C/32) contiguous 32-row blocks (1-D bulk copies, up to
-// 32 KB) into a kWideRing-slot SMEM ring, running up to kWideRing-1 blocks (across steps)
-// ahead of the consumers, so ~160 KB of l is in flight per SM independently of registers.
-// Forward: thread (j, q) takes rows q, q+4, ... of each block (8 terms, online LSE);
-// backward: warp w takes row w of each block (lanes along j).  Each warp releases a slot
-// with one arrival on its `empty` barrier (count 32).
+// A producer warp streams each tile as ceil(C/32) contiguous 32-row blocks (1-D bulk
+// copies, up to 32 KB) into a kWideRing-slot SMEM ring, across steps, as fast as the 16
+// consumer warps free slots, so up to ~190 KB of l is in flight per SM independently of
+// registers.  Forward: thread (j, q) takes rows q, q+2, ... of each block (16 terms, online
+// LSE); backward: warp w takes rows w and w+16 of each block (lanes along j).  Each consumer
+// warp releases a slot with one arrival on its `empty` barrier (count 16).
 constexpr int kWideRing = 6;
 
 __device__ __forceinline__ void wide_issue(const SemiArgs& a, int64_t b, bool fwd, int64_t Eb,
@@ -285,10 +286,14 @@ __device__ __forceinline__ void wide_issue(const SemiArgs& a, int64_t b, bool fw
   bulk_load(ring + (size_t)slot * 32 * C, src, (uint32_t)(rows * C * 4), &full[slot]);
 }
 
-__global__ void __launch_bounds__(kWideThreads, 1) fb_wide_ring_kernel(SemiArgs a) {
+constexpr int kRingConsumers = 512;                  // 16 consumer warps
+constexpr int kRingThreads = kRingConsumers + 32;    // + 1 producer warp
+constexpr int kRingCW = kRingConsumers / 32;
+
+__global__ void __launch_bounds__(kRingThreads, 1) fb_wide_ring_kernel(SemiArgs a) {
   extern __shared__ __align__(128) float wring[];
   __shared__ float vec[2][kWideMaxC];
-  __shared__ float pm[4][kWideMaxC], ps[4][kWideMaxC];
+  __shared__ float pm[2][kWideMaxC], ps[2][kWideMaxC];
   __shared__ float red[32];
   __shared__ unsigned sbad;
   __shared__ __align__(8) uint64_t full[kWideRing], empty[kWideRing];
@@ -320,13 +325,18 @@ __global__ void __launch_bounds__(kWideThreads, 1) fb_wide_ring_kernel(SemiArgs 
     vo[n0] = 0.0;
     for (int k = 0; k < kWideRing; ++k) {
       mbar_init(&full[k], 1);
-      mbar_init(&empty[k], 32);
+      mbar_init(&empty[k], kRingCW);
     }
     fence_mbar_init();
   }
   __syncthreads();
-  if (tid == 0)
-    for (int64_t h = 0; h < kWideRing - 1; ++h) wide_issue(a, b, fwd, Eb, nblk, h, wring, full, empty);
+  if (w == kRingCW) {  // producer warp: stream every block of every step through the ring
+    if (lane == 0) {
+      const int64_t total = Eb * nblk;
+      for (int64_t h = 0; h < total; ++h) wide_issue(a, b, fwd, Eb, nblk, h, wring, full, empty);
+    }
+    return;
+  }
   bool bad = false;
   double off = 0.0;
   bool dead = false;
@@ -336,44 +346,46 @@ __global__ void __launch_bounds__(kWideThreads, 1) fb_wide_ring_kernel(SemiArgs 
     const float* v = vec[(s - 1) & 1];
     float* vn = vec[s & 1];
     float val = neg_inf();
-    const int j = tid & (kWideMaxC - 1), q = tid >> 8;
+    const int j = tid & (kWideMaxC - 1), q = tid >> 8;  // q in {0, 1}: rows = q (mod 2)
     float m = neg_inf(), sum = 0.f;
     for (int kb = 0; kb < nblk; ++kb, ++g) {
-      if (tid == 0) wide_issue(a, b, fwd, Eb, nblk, g + kWideRing - 1, wring, full, empty);
       const int slot = (int)(g % kWideRing);
       mbar_wait(&full[slot], (uint32_t)((g / kWideRing) & 1));
       const float* blk = wring + (size_t)slot * 32 * C;
       const int r0 = kb * 32;
       if (fwd) {
         if (j < C) {
-          float x[8];
+          float x[16];
 #pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            const int r = q + 4 * k, i = r0 + r;
+          for (int k = 0; k < 16; ++k) {
+            const int r = q + 2 * k, i = r0 + r;
             const float lv = (i < C) ? blk[r * C + j] : neg_inf();
             bad |= (lv != lv) | (lv == pos_inf());
             x[k] = (i < C) ? fmaf(lv, kLog2e, v[i]) : neg_inf();
           }
-          online_add<8>(m, sum, x);
+          online_add<16>(m, sum, x);
         }
       } else {
-        const int i = r0 + w;
-        if (i < C) {
-          float x[kWideMaxC / 32];
-          float mm = neg_inf();
 #pragma unroll
-          for (int k = 0; k < kWideMaxC / 32; ++k) {
-            const int jj = lane + 32 * k;
-            x[k] = (jj < C) ? fmaf(blk[w * C + jj], kLog2e, v[jj]) : neg_inf();
-            mm = fmaxf(mm, x[k]);
+        for (int h = 0; h < 2; ++h) {  // rows w and w + 16 of the block
+          const int i = r0 + w + kRingCW * h;
+          if (i < C) {
+            float x[kWideMaxC / 32];
+            float mm = neg_inf();
+#pragma unroll
+            for (int k = 0; k < kWideMaxC / 32; ++k) {
+              const int jj = lane + 32 * k;
+              x[k] = (jj < C) ? fmaf(blk[(w + kRingCW * h) * C + jj], kLog2e, v[jj]) : neg_inf();
+              mm = fmaxf(mm, x[k]);
+            }
+            mm = warp_max(mm);
+            float ss = 0.f;
+            if (mm != neg_inf())
+#pragma unroll
+              for (int k = 0; k < kWideMaxC / 32; ++k) ss += ex2(x[k] - mm);
+            ss = warp_sum(ss);
+            if (lane == 0) pm[0][i] = (mm == neg_inf()) ? neg_inf() : mm + lg2(ss);
           }
-          mm = warp_max(mm);  // row max first: one ex2 per term, no online merges
-          float ss = 0.f;
-          if (mm != neg_inf())
-#pragma unroll
-            for (int k = 0; k < kWideMaxC / 32; ++k) ss += ex2(x[k] - mm);
-          ss = warp_sum(ss);
-          if (lane == 0) pm[0][i] = (mm == neg_inf()) ? neg_inf() : mm + lg2(ss);
         }
       }
       __syncwarp();
@@ -383,12 +395,11 @@ __global__ void __launch_bounds__(kWideThreads, 1) fb_wide_ring_kernel(SemiArgs 
       pm[q][j] = m;
       ps[q][j] = sum;
     }
-    __syncthreads();
+    named_bar(1, kRingConsumers);
     if (tid < C) {
       if (fwd) {
         float M = pm[0][tid], S = ps[0][tid];
-#pragma unroll
-        for (int k = 1; k < 4; ++k) lse_merge(M, S, pm[k][tid], ps[k][tid]);
+        lse_merge(M, S, pm[1][tid], ps[1][tid]);
         val = (M == neg_inf()) ? neg_inf() : M + lg2(S);
       } else {
         val = pm[0][tid];
@@ -398,7 +409,7 @@ __global__ void __launch_bounds__(kWideThreads, 1) fb_wide_ring_kernel(SemiArgs 
       const float wm = warp_max(val);
       if (lane == 0) red[w] = wm;
     }
-    __syncthreads();
+    named_bar(1, kRingConsumers);
     float Mx = red[0];
 #pragma unroll
     for (int k = 1; k < kWideMaxC / 32; ++k) Mx = fmaxf(Mx, red[k]);
@@ -410,11 +421,11 @@ __global__ void __launch_bounds__(kWideThreads, 1) fb_wide_ring_kernel(SemiArgs 
     }
     if (!dead) off += (double)Mx;
     if (tid == 0) vo[p] = dead ? -INFINITY : off;
-    __syncthreads();
+    named_bar(1, kRingConsumers);
   }
   if (!fwd) return;
   if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&sbad, 1u);
-  __syncthreads();
+  named_bar(1, kRingConsumers);
   if (tid < 32) {
     const float* vE = vec[Eb & 1];
     float sum = 0.f;
@@ -451,7 +462,7 @@ cudaError_t launch_fb_wide(const SemiArgs& a, cudaStream_t st) {
                            (int)((size_t)kWideRing * 32 * kWideMaxC * sizeof(float)));
       attr = true;
     }
-    fb_wide_ring_kernel<<<grid, kWideThreads, smem, st>>>(a);
+    fb_wide_ring_kernel<<<grid, kRingThreads, smem, st>>>(a);
   } else {
     fb_wide_sweep_kernel<<<grid, kWideThreads, 0, st>>>(a);
   }
