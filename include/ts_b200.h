@@ -237,7 +237,17 @@ TS_API ts_status ts_sample(const ts_chain *c, const float *uniforms, int64_t K, 
  * back overlaps chunk k+1's kernels and copy in).  A repeated call with the same I/O
  * binding (all pointers, sizes, semiring, workspace) replays a CUDA graph of the whole
  * pipeline captured on its second sighting (ts_set_host_graphs(0) disables this); every
- * copy and kernel still runs on every call.  Thread-safe (one lock per device). */
+ * copy and kernel still runs on every call.  Thread-safe (one lock per device).
+ * Payloads below 4 MB (one chunk) are pipelined ACROSS calls instead: the inputs are copied
+ * on a library stream into one of two device staging buffers (alternating per call), so
+ * call k's copy-in overlaps call k-1's copy-back on `stream` (PCIe is full duplex); the
+ * scan and the copy-back stay ordered on `stream` after the copy-in.  Contract of that
+ * mode: the host inputs must be ready when the call is made and must not alias the host
+ * outputs of an earlier call still in flight; the copy-in is ordered after the previous
+ * call that used the same staging buffer (and, for each buffer's first use, after the work
+ * already on `stream`), not after other work enqueued on `stream` in between — so `ws`
+ * must not be shared with other calls while pipelined calls may be in flight.
+ * ts_set_host_pipeline(0) restores plain stream order. */
 TS_API ts_status ts_marginals_host(const ts_chain *host_chain, ts_semiring s, float *host_marg,
                                    float *host_logz, uint32_t *host_flags, void *ws,
                                    size_t ws_bytes, void *stream);
@@ -245,6 +255,10 @@ TS_API ts_status ts_marginals_host(const ts_chain *host_chain, ts_semiring s, fl
 /* Debug/testing: 1 (default) = graph replay of repeated ts_marginals_host bindings,
  * 0 = always enqueue eagerly. */
 TS_API void ts_set_host_graphs(int on);
+
+/* Debug/testing: 1 (default) = the cross-call copy pipeline of ts_marginals_host for
+ * single-chunk payloads (see there), 0 = every call fully ordered on its stream. */
+TS_API void ts_set_host_pipeline(int on);
 
 /* Debug/testing: leaf chunk summaries of the time-chunked scan for 64 < C <= 128 run on
  * the tensor cores (tcgen05 kind::tf32): 3 = 3xTF32 split (default), 1 = one TF32 pass,

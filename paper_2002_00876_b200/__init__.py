@@ -60,9 +60,9 @@ class Workspace:
         self.buf = torch.empty(0, dtype=torch.uint8, device=self.device)
 
     @classmethod
-    def get(cls, device) -> "Workspace":
+    def get(cls, device, tag: str = "") -> "Workspace":
         d = torch.device(device)
-        key = (d.type, d.index if d.index is not None else torch.cuda.current_device())
+        key = (d.type, d.index if d.index is not None else torch.cuda.current_device(), tag)
         ws = cls._per_device.get(key)
         if ws is None:
             ws = cls._per_device[key] = Workspace(d)
@@ -237,7 +237,9 @@ def marginals_host(pot_host: torch.Tensor, marg_host: torch.Tensor, logz_host: t
     if need is None:
         need = _HOST_NEED[key] = int(L.ts_workspace_bytes(ctypes.byref(ch), _lib.TS_OP_MARG_HOST,
                                                           semi))
-    ws = ws or Workspace.get(device)
+    # a workspace of its own: the cross-call copy pipeline writes the next call's input
+    # staging while earlier work on the stream may still run (include/ts_b200.h)
+    ws = ws or Workspace.get(device, "host")
     wp = ws.ptr(need)
     _lib.check(L.ts_marginals_host(ctypes.byref(ch), semi, marg_host.data_ptr(),
                                    logz_host.data_ptr(),
@@ -283,6 +285,11 @@ def set_tc_summary(mode: int) -> None:
 
 def get_tc_summary() -> int:
     return int(_lib.load().ts_get_tc_summary())
+
+
+def set_host_pipeline(enable: bool) -> None:
+    """Debug knob: cross-call copy pipeline of marginals_host for single-chunk payloads."""
+    _lib.load().ts_set_host_pipeline(1 if enable else 0)
 
 
 def set_host_graphs(enable: bool) -> None:

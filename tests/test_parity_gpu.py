@@ -339,6 +339,52 @@ def test_host_buffers_end_to_end(dev, shape, graphs):
         tsb.set_host_graphs(True)
 
 
+@pytest.mark.parametrize("pipeline", [True, False])
+def test_host_pipeline_back_to_back(dev, pipeline):
+    """Cross-call copy pipeline of ts_marginals_host (single-chunk payloads): 6 calls
+    enqueued back to back WITHOUT synchronising, alternating between two input/output
+    buffer sets and rewriting host inputs only after the call that read them completed,
+    with and without graph replay; every result matches the oracle."""
+    B, N, C = 32, 25, 20
+    sets = []
+    for _ in range(3):
+        sets.append(tuple(torch.empty(sh, dtype=dt).pin_memory() for sh, dt in
+                          [((B, N - 1, C, C), torch.float32), ((B, N - 1, C, C), torch.float32),
+                           ((B,), torch.float32), ((B,), torch.int32)]))
+    refs = {}
+    tsb.set_host_pipeline(pipeline)
+    try:
+        for graphs in (True, False):
+            tsb.set_host_graphs(graphs)
+            events = []
+            for call in range(6):
+                pot, marg, logz, flags = sets[call % 3]
+                if call >= 3:
+                    events[call - 3].synchronize()   # the call that read this input is done
+                    k = call - 3
+                    lz_ref, mg_ref, fl_ref = refs[k]
+                    p_, m_, l_, f_ = sets[k % 3]
+                    check_logz(l_.numpy(), lz_ref)
+                    check_marg(m_.numpy(), mg_ref)
+                    np.testing.assert_array_equal(f_.numpy(), fl_ref)
+                pot_np = tsgen.potentials(B, N, C, seed=500 + call + 10 * graphs)
+                pot.copy_(torch.from_numpy(pot_np))
+                refs[call] = oracle.chain_marginals(pot_np)
+                tsb.marginals_host(pot, marg, logz, flags, device=dev)
+                ev = torch.cuda.Event()
+                ev.record()
+                events.append(ev)
+            torch.cuda.synchronize()
+            for k in range(3, 6):
+                lz_ref, mg_ref, fl_ref = refs[k]
+                p_, m_, l_, f_ = sets[k % 3]
+                check_logz(l_.numpy(), lz_ref)
+                check_marg(m_.numpy(), mg_ref)
+    finally:
+        tsb.set_host_graphs(True)
+        tsb.set_host_pipeline(True)
+
+
 @pytest.mark.parametrize("G", [2, 4])
 def test_cluster_dsmem_variant(dev, G):
     """The chunked-scan variant for short chains on a G-CTA cluster (DSMEM summary exchange)."""
