@@ -65,7 +65,10 @@ __device__ long long g_tiny_edge[64][4];   // cta 0 per edge: waited, summed, st
 
 namespace {
 
-constexpr int kTinyThreads = 512;
+#ifndef TINY_THREADS
+#define TINY_THREADS 384  // swept 256-1024 (bench cfg2): 384 best, 6.66 vs 6.71 us/step at 512
+#endif
+constexpr int kTinyThreads = TINY_THREADS;
 constexpr int kTinyWarps = kTinyThreads / 32;
 // Recursion warps.  Warp 0 is avoided: a recursion on warp 0 measured ~4x slower per step
 // (938 vs 226 cycles at C = 20, tools/phase_tiny.cu) for reasons not yet understood.
