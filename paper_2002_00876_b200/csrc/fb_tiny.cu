@@ -73,10 +73,10 @@ constexpr int kTinyWarps = kTinyThreads / 32;
 // Recursion warps.  Warp 0 is avoided: a recursion on warp 0 measured ~4x slower per step
 // (938 vs 226 cycles at C = 20, tools/phase_tiny.cu) for reasons not yet understood.
 #ifndef TINY_FWD_WARP
-#define TINY_FWD_WARP 1
+#define TINY_FWD_WARP 2  // (fwd, bwd) warps swept at 384 threads: (2,3) 6.62 vs (1,2) 6.66 us/step
 #endif
 #ifndef TINY_BWD_WARP
-#define TINY_BWD_WARP 2
+#define TINY_BWD_WARP 3
 #endif
 constexpr int kFwdWarp = TINY_FWD_WARP;            // forward recursion
 constexpr int kBwdWarp = TINY_BWD_WARP;            // backward recursion
