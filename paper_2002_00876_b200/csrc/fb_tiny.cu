@@ -325,6 +325,16 @@ __global__ void __launch_bounds__(kTinyThreads, 1) fb_tiny_kernel(SmallArgs a) {
   // programmatic dependent launch: the next kernel in the stream may start its prologue now;
   // this kernel touches global memory only after the previous grid has completed
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#ifndef TINY_NO_L2_PREFETCH
+  // While the previous grid drains, warm L2 with this sequence's tiles (all N-1 edges, so no
+  // input is read yet): a prefetch is only a hint and L2 is the coherence point, so a tile
+  // the previous grid might still write cannot be observed stale.
+  if (lane == 0 && a.pot)
+    for (int64_t t = warp; t < E; t += kTinyWarps)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.pot + (b * E + t) * CC),
+                   "r"((uint32_t)(CC * 4))
+                   : "memory");
+#endif
   asm volatile("griddepcontrol.wait;" ::: "memory");
   __syncthreads();
 
