@@ -246,7 +246,9 @@ TS_API ts_status ts_sample(const ts_chain *c, const float *uniforms, int64_t K, 
  * outputs of an earlier call still in flight; the copy-in is ordered after the previous
  * call that used the same staging buffer (and, for each buffer's first use, after the work
  * already on `stream`), not after other work enqueued on `stream` in between — so `ws`
- * must not be shared with other calls while pipelined calls may be in flight.
+ * must not be shared with calls of OTHER entry points while pipelined calls may be in
+ * flight.  A change of binding (B, N, C, ws, semiring) or an intervening stream-ordered
+ * ts_marginals_host call re-orders the next copy-in after all work on `stream`.
  * ts_set_host_pipeline(0) restores plain stream order. */
 TS_API ts_status ts_marginals_host(const ts_chain *host_chain, ts_semiring s, float *host_marg,
                                    float *host_logz, uint32_t *host_flags, void *ws,

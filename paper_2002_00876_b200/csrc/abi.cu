@@ -517,6 +517,7 @@ struct HostPipe {
   cudaEvent_t ev_in[2], ev_done[2];
   int parity = 0;
   bool primed[2] = {false, false};
+  int64_t sig[5] = {0, 0, 0, 0, 0};  // (B, N, C, ws, semiring) of the last pipelined call
   HostGraph graphs[kHostGraphs];
   int n_graphs = 0;
   uint64_t clock = 0;
@@ -1125,6 +1126,13 @@ static ts_status host_pipelined(HostPipe* hp, const ts_chain* hc, ts_semiring s,
   void* inner = cv.take<char>(inner_bytes);
   float* d_pot1 = cv.take<float>(nel);
   int32_t* d_len1 = cv.take<int32_t>((size_t)B);
+  // a different binding lays the workspace out differently: order this call's copy-in after
+  // everything on `st` (the staging buffers of the new layout may overlap the old one's)
+  const int64_t sig[5] = {B, N, C, (int64_t)reinterpret_cast<uintptr_t>(ws), (int64_t)s};
+  if (std::memcmp(sig, hp->sig, sizeof sig) != 0) {
+    std::memcpy(hp->sig, sig, sizeof sig);
+    hp->primed[0] = hp->primed[1] = false;
+  }
   const int p = hp->parity;
   hp->parity ^= 1;
   float* d_pot = p ? d_pot1 : d_pot0;
@@ -1203,6 +1211,8 @@ TS_API ts_status ts_marginals_host(const ts_chain* hc, ts_semiring s, float* hos
   std::lock_guard<std::mutex> lock(hp->mu);
   if (g_host_pipeline.load() && host_chunks(hc->B, (hc->N - 1) * hc->C * hc->C) == 1)
     return host_pipelined(hp, hc, s, host_marg, host_logz, host_flags, ws, ws_bytes, st);
+  // a stream-ordered call: the next pipelined call must order its copy-in after it again
+  hp->primed[0] = hp->primed[1] = false;
   // Replay path: the same I/O binding seen before -> one graph launch (all copies and
   // kernels of the call are nodes of the instantiated graph; nothing is skipped).
   HostKey key{hc->B, hc->N, hc->C, hc->pot, hc->lengths, (int)s, host_marg, host_logz,

@@ -385,6 +385,28 @@ def test_host_pipeline_back_to_back(dev, pipeline):
         tsb.set_host_pipeline(True)
 
 
+def test_host_pipeline_binding_changes(dev):
+    """Pipelined host calls interleaved with calls of other shapes (a different workspace
+    layout) on the same workspace, enqueued without synchronising: every result is right."""
+    shapes = [(32, 25, 20), (5, 40, 12), (32, 25, 20), (64, 300, 20), (32, 25, 20)]
+    ws = tsb.Workspace(dev)
+    outs = []
+    for k, (B, N, C) in enumerate(shapes):
+        pot_np = tsgen.potentials(B, N, C, seed=900 + k)
+        pot = torch.from_numpy(pot_np).pin_memory()
+        marg = torch.empty_like(pot).pin_memory()
+        logz = torch.empty(B, dtype=torch.float32).pin_memory()
+        flags = torch.empty(B, dtype=torch.int32).pin_memory()
+        tsb.marginals_host(pot, marg, logz, flags, device=dev, ws=ws)
+        outs.append((pot_np, marg, logz, flags))
+    torch.cuda.synchronize()
+    for pot_np, marg, logz, flags in outs:
+        lz_ref, mg_ref, fl_ref = oracle.chain_marginals(pot_np, None, threads=8)
+        check_logz(logz.numpy(), lz_ref)
+        check_marg(marg.numpy(), mg_ref)
+        np.testing.assert_array_equal(flags.numpy(), fl_ref)
+
+
 @pytest.mark.parametrize("G", [2, 4])
 def test_cluster_dsmem_variant(dev, G):
     """The chunked-scan variant for short chains on a G-CTA cluster (DSMEM summary exchange)."""
