@@ -78,7 +78,7 @@ enum {
   TS_OP_MARG_HOST = 3, /* ts_marginals_host (adds device staging of I/O)    */
   TS_OP_SEGMENT = 4,   /* ts_segment_summary + ts_segment_finish            */
   TS_OP_ENTROPY = 5,   /* ts_entropy (TS_LOG)                               */
-  TS_OP_SAMPLE = 6,    /* ts_sample (TS_LOG, C <= 128)                      */
+  TS_OP_SAMPLE = 6,    /* ts_sample (TS_LOG)                                */
   TS_OP_SEGMENT_VITERBI = 7, /* ts_segment_viterbi_maps + _finish (same ws)  */
   TS_OP_KBEST = 8,     /* ts_kbest: size via ts_kbest_workspace_bytes(c, K)  */
   TS_OP_EXPECTATION = 9 /* ts_expectation (TS_LOG; same size as TS_OP_ENTROPY) */
@@ -224,7 +224,8 @@ TS_API ts_status ts_log_prob(const ts_chain *c, const int32_t *z, const float *l
  * [K][B][N] fp32 in [0, 1), u[k][b][t] drives the draw of z_t (inverse CDF: the smallest
  * label whose inclusive prefix sum of p(z_t | z_{t+1}) exceeds u * total; z_{len-1} from
  * p(z_{len-1})).  z [K][B][N] int32 out (-1 beyond len and for flagged sequences); logz [B]
- * out (required); flags [B] out or NULL.  TS_LOG only, C <= 128 (TS_E_UNSUPPORTED above).
+ * out (required); flags [B] out or NULL.  TS_LOG only; C <= 128 filters with the streaming
+ * forward sweep, 128 < C <= 256 with the forward recursion of the wide-label path.
  * ws: ts_workspace_bytes(c, TS_OP_SAMPLE, TS_LOG) bytes (forward node vectors [B][N][C]). */
 TS_API ts_status ts_sample(const ts_chain *c, const float *uniforms, int64_t K, int32_t *z,
                            float *logz, uint32_t *flags, void *ws, size_t ws_bytes, void *stream);

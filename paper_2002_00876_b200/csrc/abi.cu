@@ -662,7 +662,11 @@ TS_API size_t ts_workspace_bytes(const ts_chain* c, int op, ts_semiring s) {
   if (op == TS_OP_SEGMENT_VITERBI) return c->C <= 128 ? vseg_ws(c, nullptr, nullptr) : 0;
   if (op == TS_OP_ENTROPY || op == TS_OP_EXPECTATION)
     return s == TS_LOG ? entropy_ws(c, nullptr, nullptr, nullptr) : 0;
-  if (op == TS_OP_SAMPLE) return (s == TS_LOG && c->C <= 128) ? sample_ws(c, nullptr, nullptr, nullptr) : 0;
+  if (op == TS_OP_SAMPLE) {
+    if (s != TS_LOG) return 0;
+    if (c->C <= 128) return sample_ws(c, nullptr, nullptr, nullptr);
+    return align_up(semi_ws(c, 1, nullptr, nullptr)) + align_up(sizeof(uint32_t) * (size_t)c->B);
+  }
   if (op < TS_OP_LOGZ || op > TS_OP_VITERBI) return 0;
   return op_ws(c, op, s, nullptr, nullptr, nullptr);
 }
@@ -952,9 +956,45 @@ TS_API ts_status ts_sample(const ts_chain* c, const float* uniforms, int64_t K, 
   if (!chain_ok(c) || !uniforms || !aligned(uniforms, 4) || K < 1 || K > ((int64_t)1 << 31) ||
       !z || !aligned(z, 4) || !logz || !aligned(logz, 4) || (flags && !aligned(flags, 4)))
     return TS_E_INVALID;
-  if (c->C > 128) return TS_E_UNSUPPORTED;
   if (!device_ok()) return TS_E_UNSUPPORTED;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (c->C > 128) {
+    // wide labels: the forward recursion of fb_wide (exact per-cell LSE) stores every node
+    // vector (log2, normalised) and writes logZ + flags; then the same backward sampler
+    SemiArgs sa{};
+    const size_t m = align_up(semi_ws(c, 1, ws, &sa));
+    const size_t need = m + align_up(sizeof(uint32_t) * (size_t)c->B);
+    if (ws_bytes < need || !ws || !aligned(ws, kAlign)) return TS_E_WORKSPACE;
+    uint32_t* fl = flags ? flags : reinterpret_cast<uint32_t*>(static_cast<char*>(ws) + m);
+    sa.pot = c->pot;
+    sa.lengths = c->lengths;
+    sa.B = c->B;
+    sa.N = c->N;
+    sa.C = c->C;
+    sa.marg = nullptr;
+    sa.logz = logz;
+    sa.flags = fl;
+    ts_status r = cuda_status(launch_fb_wide(sa, st));
+    if (r != TS_OK) return r;
+    DistArgs d{};
+    d.pot = c->pot;
+    d.lengths = c->lengths;
+    d.B = c->B;
+    d.N = c->N;
+    d.C = c->C;
+    d.flags = fl;
+    d.zout = z;
+    d.uniforms = uniforms;
+    d.K = K;
+    d.ah = sa.ah;
+    d.aend_in_ah = 1;
+    r = cuda_status(launch_sample(d, st));
+    if (r == TS_OK) {
+      t_launches = 2;
+      t_kernel = "sample_kernel";
+    }
+    return r;
+  }
   StreamWs w;
   uint32_t* wfl = nullptr;
   const size_t need = sample_ws(c, ws, &w, &wfl);

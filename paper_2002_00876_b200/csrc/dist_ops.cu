@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(128) sample_kernel(DistArgs a) {
   const int i0 = R * lane;
   float lw[R];
   // z_{len-1} ~ 2^(ah_{len-1}[j])
-  const float* v = a.aend + b * C;
+  const float* v = a.aend_in_ah ? a.ah + (b * N + len - 1) * C : a.aend + b * C;
   if (len - 1 == 0) {  // single node: every label has weight 1 (alpha_0 = 0)
 #pragma unroll
     for (int r = 0; r < R; ++r) lw[r] = (i0 + r < C) ? 0.f : neg_inf();

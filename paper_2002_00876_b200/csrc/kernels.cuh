@@ -170,6 +170,7 @@ struct DistArgs {
   int64_t K;
   const float* ah;         // sample: forward node vectors [B][N][C] (log2, per-node frame)
   const float* aend;       // sample: node Eb vector [B][C]
+  int aend_in_ah;          // sample: node len-1 vector is row len-1 of ah (fb_wide, C > 128)
 };
 int entropy_slices(const DistArgs& a);
 cudaError_t launch_entropy(DistArgs a, cudaStream_t st);

@@ -154,7 +154,8 @@ def test_next_row_workspace_sizes():
                                 _lib.TS_MAX) >= 4 * 99 * 20
     assert L.ts_semimarkov_workspace_bytes(ctypes.byref(ch), 4) >= 2 * 4 * 100 * 20 * 4
     big = _chain(B=4, N=100, C=200)
-    assert L.ts_workspace_bytes(ctypes.byref(big), _lib.TS_OP_SAMPLE, _lib.TS_LOG) == 0
+    # sampling for 128 < C <= 256 filters with the wide-label recursion (node vectors in ws)
+    assert L.ts_workspace_bytes(ctypes.byref(big), _lib.TS_OP_SAMPLE, _lib.TS_LOG) >= 4 * 100 * 200 * 4
     assert L.ts_semimarkov_workspace_bytes(ctypes.byref(big), 4) >= 2 * 4 * 100 * 200 * 4
-    # the log semiring for long chains with 128 < C <= 256 runs the exact SIMT kernel
+    # the log semiring for long chains with 128 < C <= 256 runs fb_wide (node vectors in ws)
     assert L.ts_workspace_bytes(ctypes.byref(big), _lib.TS_OP_MARG, _lib.TS_LOG) >= 2 * 4 * 100 * 200 * 4

@@ -165,7 +165,8 @@ def _oracle_margin(pot_seq, n, zpath, u, t):
     return float(np.min(np.abs(c - u * c[-1])) / c[-1])
 
 
-@pytest.mark.parametrize("B,N,C", [(3, 40, 20), (2, 60, 64), (2, 30, 128), (4, 25, 7)])
+@pytest.mark.parametrize("B,N,C", [(3, 40, 20), (2, 60, 64), (2, 30, 128), (4, 25, 7),
+                                   (2, 30, 200), (2, 20, 256), (2, 15, 131)])
 def test_sampling_matches_oracle_paths(dev, B, N, C):
     K = 8
     pot = tsgen.potentials(B, N, C, seed=6000 + N + C)
@@ -185,6 +186,25 @@ def test_sampling_matches_oracle_paths(dev, B, N, C):
             m = _oracle_margin(pot[b], N, ref[k, b], float(u[k, b, t]), t)
             assert m < 1e-4, (k, b, t, m)
     assert same >= 0.9 * K * B, same
+
+
+def test_sampling_wide_labels_lengths_flags(dev):
+    """128 < C <= 256 (forward filtering through the wide-label recursion): lengths, len 1,
+    EMPTY and BADLEN rows behave as for narrow labels."""
+    B, N, C = 5, 12, 160
+    pot = tsgen.potentials(B, N, C, seed=18)
+    lengths = np.array([N, 1, 5, 0, N], np.int32)
+    pot[4] = -np.inf
+    u = np.random.default_rng(3).random((3, B, N)).astype(np.float32)
+    z, lz, fl = tsb.sample(_dev(pot, dev), _dev(u, dev), _dev(lengths, dev))
+    z = z.cpu().numpy()
+    ref = oracle.ffbs_sample(pot, u.astype(np.float64), lengths)
+    assert (z[:, 3] == -1).all() and (z[:, 4] == -1).all()
+    assert (z[:, 2, 5:] == -1).all() and (z[:, 1, 1:] == -1).all()
+    np.testing.assert_array_equal(z[:, 1, 0], ref[:, 1, 0])
+    assert (fl.cpu().numpy()[[3, 4]] != 0).all()
+    lz_ref, _, _ = oracle.chain_marginals(pot, lengths, want_marg=False)
+    check_logz(lz.cpu().numpy()[[0, 1, 2]], lz_ref[[0, 1, 2]])
 
 
 def test_sampling_lengths_flags(dev):
