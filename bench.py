@@ -6,7 +6,17 @@ JSON line on rank 0.  A step = one ts_marginals call (the whole hot path: forwar
 explicit backward scan, marginals, logZ) over one batch of the BASELINE.json metric
 workload: B=32, N=25, C=20 (Table 1 caption), synthetic seeded
 dyadic potentials (tsgen).  Multi-GPU: one process per GPU, each rank its own B=32
-batch (weak scaling, no data-path collective); time = max over ranks.
+batch (weak scaling, no data-path collective); time = max over ranks.  Run without
+torchrun and with --gpus N > 1, the script re-launches itself under torchrun with N ranks.
+
+Cold L2: inputs/outputs rotate over R buffer sets with R·set > 2·L2; the
+timed graph of K calls is always preceded (untimed) by a graph of the R calls that come
+before it in the rotation, so every timed call's buffers were last touched R calls earlier
+whatever K is.
+
+The same line carries the other BASELINE configs as side measurements ("side": cfg3 and
+cfg5 logZ + marginals, cfg4 Viterbi; batch-sharded per rank for cfg3/cfg4 and time-sharded
+with one NCCL all-gather for cfg5 when N > 1), each with its own clock record.
 
 `--impl reference` times the fp64 CPU oracle (oracle/) on the host cores as the
 reference arm (this tier has no runnable upstream implementation).
@@ -16,6 +26,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -34,6 +45,41 @@ def env_rank():
             int(os.environ.get("WORLD_SIZE", 1)))
 
 
+def free_port() -> int:
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def maybe_spawn(argv, gpus: int):
+    """`python bench.py --gpus N` (N > 1) outside torchrun: re-launch under torchrun with N
+    ranks on this node (127.0.0.1 rendezvous).  Returns the exit code, or None when this
+    process is already a rank (or N == 1)."""
+    if gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={free_port()}", os.path.abspath(__file__)] + list(argv)
+    env = dict(os.environ)
+    env.setdefault("OMP_NUM_THREADS", "1")
+    return subprocess.call(cmd, env=env)
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def host_cores() -> int:
+    return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -44,13 +90,23 @@ def load_peaks():
 
 
 def load_traffic(kernel: str, cfg_no: int):
+    """DRAM bytes per launch of `kernel` from the committed ncu --set full capture."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not os.path.exists(p):
-        return None
+        return None, None
     with open(p) as f:
         d = json.load(f)
     v = d.get(f"cfg{cfg_no}", {}).get(kernel)
-    return None if v is None else float(v)
+    return (None if v is None else float(v)), d.get("source")
+
+
+def pctl(xs, q):
+    xs = sorted(xs)
+    if not xs:
+        return None
+    k = (len(xs) - 1) * q
+    lo, hi = int(k), min(int(k) + 1, len(xs) - 1)
+    return xs[lo] + (xs[hi] - xs[lo]) * (k - lo)
 
 
 class ClockSampler:
@@ -74,9 +130,10 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
-            return
+            return self
         self.th = threading.Thread(target=self._read, daemon=True)
         self.th.start()
+        return self
 
     def _read(self):
         for line in self.proc.stdout:
@@ -93,6 +150,7 @@ class ClockSampler:
                 self.proc.kill()
         if self.th is not None:
             self.th.join(timeout=2)
+        return self
 
     def summary(self):
         if not self.rows:
@@ -106,14 +164,15 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
+# ------------------------------------------------------------------------ reference arm
+
 def oracle_baseline(cfg, seconds: float = 8.0, max_batches: int = 2000):
     """Time the fp64 oracle (as it stands) on this host: whole cfg batches, threads across b."""
     import oracle
     import tsgen
 
     pot = tsgen.config_potentials(cfg)
-    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
-    threads = max(1, min(cfg.B, cores))
+    threads = max(1, min(cfg.B, host_cores()))
     oracle.chain_marginals(pot, threads=threads)  # warm (library load)
     n = 0
     t0 = time.perf_counter()
@@ -124,6 +183,7 @@ def oracle_baseline(cfg, seconds: float = 8.0, max_batches: int = 2000):
         if el >= seconds or n >= max_batches:
             break
     return {"value": n * cfg.tokens / el, "unit": UNIT, "cores": threads, "kind": "oracle",
+            "cpu": cpu_model(), "host_cores": host_cores(),
             "sample": f"{n} batches of B={cfg.B} N={cfg.N} C={cfg.C} (fp64 forward-backward + "
                       f"marginals, {el:.1f} s wall)"}
 
@@ -137,8 +197,7 @@ def run_reference(args):
 
     cfg = tsgen.CONFIGS[args.config]
     pot = tsgen.config_potentials(cfg)
-    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
-    threads = max(1, min(cfg.B, cores))
+    threads = max(1, min(cfg.B, host_cores()))
     for _ in range(args.warmup):
         oracle.chain_marginals(pot, threads=threads)
     t0 = time.perf_counter()
@@ -150,136 +209,170 @@ def run_reference(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (tsgen seeded dyadic potentials)",
-            "config": {"workload": f"cfg{cfg.no}: {cfg.label}", "B": cfg.B, "N": cfg.N,
-                       "C": cfg.C, "parallelism": "host threads across the batch"},
+            "config": cfg_dict(cfg, args.gpus, "host threads across the batch (oracle, rank 0)"),
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle",
+                             "cpu": cpu_model(), "host_cores": host_cores(),
                              "sample": f"{args.steps} batches of B={cfg.B} N={cfg.N} C={cfg.C}"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
 
 
-def run_time_sharded(args):
-    """Side mode (not the driver's line): cfg5-style long chains split in TIME across the
-    ranks (DESIGN.md §6): each rank generates its edge range in place, runs the local scan
-    summary, one NCCL all_gather_into_tensor of the C x C summaries, then the combine and its
-    local sweeps + marginals.  Total work is fixed as N grows ("scaling": "strong").  Time =
-    max over ranks of CUDA-event time around K steps (summary + all-gather + finish)."""
-    import torch
+def cfg_dict(cfg, world, parallelism, **extra):
+    d = {"workload": f"cfg{cfg.no}: {cfg.label}", "B": cfg.B, "N": cfg.N, "C": cfg.C,
+         "global_batch": cfg.B * world, "seq_len": cfg.N, "parallelism": parallelism}
+    d.update(extra)
+    return d
 
+
+# ------------------------------------------------------------------------- GPU helpers
+
+class Ctx:
+    def __init__(self):
+        import torch
+
+        self.torch = torch
+        self.rank, self.local_rank, self.world = env_rank()
+        torch.cuda.set_device(self.local_rank)
+        self.dev = torch.device("cuda", self.local_rank)
+        self.dist = None
+        if self.world > 1:
+            import torch.distributed as dist
+
+            dist.init_process_group("nccl", device_id=self.dev)
+            self.dist = dist
+
+    def barrier(self):
+        if self.dist is not None:
+            self.dist.barrier()
+        self.torch.cuda.synchronize(self.dev)
+
+    def max_over_ranks(self, vals):
+        t = self.torch.tensor(list(vals), dtype=self.torch.float64, device=self.dev)
+        if self.dist is not None:
+            self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return [float(x) for x in t.cpu()]
+
+    def close(self):
+        if self.dist is not None:
+            self.dist.barrier()
+            self.dist.destroy_process_group()
+
+
+def timed_calls(ctx, call, reps: int, warmup: int = 3):
+    """Per-call CUDA-event times (ms) of `call()` on the current stream, each call bracketed
+    by events; returns the per-rep max over ranks."""
+    torch = ctx.torch
+    for _ in range(warmup):
+        call()
+    ctx.barrier()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(reps)]
+    for e0, e1 in evs:
+        e0.record()
+        call()
+        e1.record()
+    torch.cuda.synchronize(ctx.dev)
+    return ctx.max_over_ranks([e0.elapsed_time(e1) for e0, e1 in evs])
+
+
+def side_configs(ctx, args):
+    """cfg3 / cfg4 / cfg5 (BASELINE.json configs[2..4]) on this rank's share, each with its
+    own clock record: cfg3 logZ + marginals and cfg4 Viterbi batch-sharded (B/N per rank,
+    no collective), cfg5 logZ + marginals time-sharded over the ranks (one NCCL all-gather
+    of the segment summaries; the plain ts_marginals call at N = 1).  Inputs are larger
+    than L2 (2.1 / 17.2 / 17.2 GB in total), so no rotation is needed."""
     import paper_2002_00876_b200 as tsb
     import tsgen
     from paper_2002_00876_b200 import dist as tdist
 
-    rank, local_rank, world = env_rank()
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
+    torch = ctx.torch
+    peak, _ = load_peaks()
+    out = {}
+    for no in args.side:
+        cfg = tsgen.CONFIGS[no]
+        B, N, C, E = cfg.B, cfg.N, cfg.C, cfg.E
+        sampler = ClockSampler(ctx.local_rank)
+        if no in (3, 4):
+            b0, b1 = tdist.shard_batch(B, ctx.world, ctx.rank)
+            nb = b1 - b0
+            pot = torch.empty((nb, E, C, C), dtype=torch.float32, device=ctx.dev)
+            tsgen.fill_torch_batch(pot, cfg, b0)
+            ws = tsb.Workspace(ctx.dev)
+            if cfg.op == "viterbi":
+                def call():
+                    tsb.viterbi(pot, ws=ws)
+                alg = 4 * B * E * C * C
+                kern_of = "viterbi"
+            else:
+                marg = torch.empty_like(pot)
 
-        dist.init_process_group("nccl", device_id=dev)
-    cfg = tsgen.CONFIGS[args.config]
-    B, N, C, E = cfg.B, cfg.N, cfg.C, cfg.E
-    begin, count = tdist.shard_edges(E, world, rank)
-    local = torch.empty((B, count, C, C), dtype=torch.float32, device=dev)
-    tsgen.fill_torch(local, cfg.seed, cfg.quantum, t_begin=begin, E_global=E)
-    seg = tsb.Segment(local, begin, N)
-    marg = None
+                def call():
+                    tsb.marginals(pot, ws=ws, out=marg)
+                alg = 8 * B * E * C * C
+                kern_of = "marginals"
+            call()
+            kernel, launches = tsb.last_kernel(), tsb.last_launch_count()
+            par = f"batch-sharded: B={nb} of {B} on this rank, no collective"
+        else:
+            begin, count = tdist.shard_edges(E, ctx.world, ctx.rank)
+            pot = torch.empty((B, count, C, C), dtype=torch.float32, device=ctx.dev)
+            tsgen.fill_torch(pot, cfg.seed, cfg.quantum, t_begin=begin, E_global=E)
+            alg = 8 * B * E * C * C
+            kern_of = "marginals"
+            if ctx.world == 1:
+                ws = tsb.Workspace(ctx.dev)
+                marg = torch.empty_like(pot)
 
-    def step():
-        nonlocal marg
-        summ = seg.summary()
-        gathered = tdist._all_gather(summ, None) if dist is not None else summ[None]
-        marg, logz, flags = seg.finish(gathered, rank, world, True)
-        return logz, flags
+                def call():
+                    tsb.marginals(pot, ws=ws, out=marg)
+                par = "one GPU: time-chunked scan (ts_marginals)"
+            else:
+                seg = tsb.Segment(pot, begin, N)
 
-    for _ in range(args.warmup):
-        logz, flags = step()
-    torch.cuda.synchronize(dev)
-    assert int(flags.abs().sum()) == 0
-    if dist is not None:
-        dist.barrier()
-    torch.cuda.synchronize(dev)
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    sampler = ClockSampler(local_rank)
-    sampler.start()
-    ev0.record()
-    for _ in range(args.steps):
-        step()
-    ev1.record()
-    torch.cuda.synchronize(dev)
-    sampler.stop()
-    ms_t = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device=dev)
-    if dist is not None:
-        dist.barrier()
-        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
-    ms = float(ms_t.item()) / args.steps
-    if rank == 0:
-        peak, peak_src = load_peaks()
-        alg = 8 * B * E * C * C
-        line = {"metric": f"tokens/sec linear-chain logZ+marginals time-sharded (cfg{cfg.no}: "
-                          f"B={B},N={N},C={C})", "value": B * N / (ms / 1e3), "unit": UNIT,
-                "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-                "dtype": "f32", "data": "synthetic (tsgen, generated in place per rank)",
-                "config": {"workload": f"cfg{cfg.no}: {cfg.label}",
-                           "parallelism": f"time-sharded over {world} GPU(s), one NCCL "
-                                          "all_gather of C x C segment summaries per step",
-                           "l2": f"inputs {alg / 2 / 1e9:.1f} GB >> L2"},
-                "roofline": {"bound": "hbm", "achieved": alg / (ms / 1e3) / 1e9 / world,
-                             "peak": peak, "unit": "GB/s (per GPU)",
-                             "frac": alg / (ms / 1e3) / 1e9 / world / peak,
-                             "peak_source": peak_src},
-                "clocks": sampler.summary()}
-        print(json.dumps(line), flush=True)
-    if dist is not None:
-        dist.barrier()
-        dist.destroy_process_group()
-    return 0
+                def call():
+                    summ = seg.summary()
+                    seg.finish(tdist._all_gather(summ, None), ctx.rank, ctx.world, True)
+                par = (f"time-sharded over {ctx.world} GPUs: local scan + one NCCL all_gather "
+                       "of C x C segment summaries + combine + local sweeps")
+            call()
+            kernel, launches = tsb.last_kernel(), tsb.last_launch_count()
+        sampler.start()
+        ms = timed_calls(ctx, call, reps=args.side_reps)
+        sampler.stop()
+        med = statistics.median(ms)
+        ach = alg / (med / 1e3) / 1e9 / ctx.world
+        out[f"cfg{no}"] = {
+            "op": kern_of, "B": B, "N": N, "C": C, "parallelism": par,
+            "ms_median": med, "ms_p10": pctl(ms, 0.1), "ms_p90": pctl(ms, 0.9), "reps": len(ms),
+            "tokens_per_s": B * N / (med / 1e3),
+            "roofline": {"bound": "hbm", "alg_bytes": alg, "achieved_gbs_per_gpu": ach,
+                         "peak": peak, "frac": ach / peak},
+            "dominant_kernel": kernel, "launches_per_call": launches,
+            "clocks": sampler.summary()}
+        del pot
+        torch.cuda.empty_cache()
+    return out
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=2000)
-    ap.add_argument("--warmup", type=int, default=50)
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=2)
-    ap.add_argument("--mode", default="graph", choices=["graph", "eager"])
-    ap.add_argument("--sets", type=int, default=0, help="rotating buffer sets (0 = auto > 2x L2)")
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=0)
-    ap.add_argument("--time-shard", action="store_true",
-                    help="side mode: time-sharded long chains (use with --config 5)")
-    ap.add_argument("--tiny-mode", type=int, default=-1,
-                    help="debug: cfg2 kernel variant (ts_set_tiny: 1 default, 0 general kernel)")
-    args = ap.parse_args()
-    args.warmup = max(args.warmup, 3)
-    if args.impl == "reference":
-        return run_reference(args)
-    if args.time_shard:
-        return run_time_sharded(args)
+# ------------------------------------------------------------------------ the main line
 
-    import torch
+def run_ours(args):
+    import ctypes
 
     import paper_2002_00876_b200 as tsb
     import tsgen
 
-    rank, local_rank, world = env_rank()
+    ctx = Ctx()
+    torch = ctx.torch
+    dev, rank, world = ctx.dev, ctx.rank, ctx.world
     if args.tiny_mode >= 0:
         tsb.set_tiny(args.tiny_mode)
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl", device_id=dev)
 
     cfg = tsgen.CONFIGS[args.config]
     assert cfg.op == "marg", "bench times logZ + marginals configs"
     B, N, C, E = cfg.B, cfg.N, cfg.C, cfg.E
+    K = args.steps
     set_bytes = 2 * B * E * C * C * 4
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     R = args.sets or max(2, int((2 * l2 + set_bytes - 1) // set_bytes))
@@ -297,8 +390,6 @@ def main():
     stream = torch.cuda.current_stream(dev)
 
     # a prepared ABI call per buffer set (argument marshalling hoisted out of the loop)
-    import ctypes
-
     L = tsb._lib.load()
     chains = [tsb._lib.ts_chain(B, N, C, p.data_ptr(), None) for p in pots]
     need = int(L.ts_workspace_bytes(ctypes.byref(chains[0]), tsb._lib.TS_OP_MARG, tsb._lib.TS_LOG))
@@ -317,57 +408,76 @@ def main():
     launches_per_step = tsb.last_launch_count()
     kernel = tsb.last_kernel()
     torch.cuda.synchronize(dev)
+    assert int(flags.abs().sum()) == 0
 
-    graph = None
-    if args.mode == "graph":
+    def capture(ks):
+        g = torch.cuda.CUDAGraph()
         side = torch.cuda.Stream(dev)
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph, stream=side):
+        with torch.cuda.graph(g, stream=side):
             h = torch.cuda.current_stream(dev).cuda_stream
-            for k in range(args.steps):
+            for k in ks:
                 step(k, h)
-        graph.replay()  # warm the instantiated graph
-        torch.cuda.synchronize(dev)
+        return g
 
-    sampler = ClockSampler(local_rank) if rank == 0 or True else None
-    sampler.start()
-    # settle clocks under this load for ~1 s (untimed), then the timed region
-    t_end = time.perf_counter() + 1.0
-    k = 0
-    while time.perf_counter() < t_end:
-        if graph is not None:
-            graph.replay()
+    # timed graph: calls 0..K-1 (sets k mod R); preroll: the R calls before call 0 in the
+    # rotation (calls -R..-1 = sets 0..R-1), so each timed set was last touched R calls ago
+    timed = capture(range(K)) if args.mode == "graph" else None
+    preroll = capture(range(-R, 0)) if args.mode == "graph" else None
+
+    def run_preroll():
+        if preroll is not None:
+            preroll.replay()
         else:
-            for _ in range(200):
+            for k in range(-R, 0):
                 step(k, st_handle)
-                k += 1
+
+    def run_timed():
+        if timed is not None:
+            timed.replay()
+        else:
+            for k in range(K):
+                step(k, st_handle)
+
+    sampler = ClockSampler(ctx.local_rank).start()
+    # settle clocks under this load for ~1 s (untimed)
+    t_end = time.perf_counter() + 1.0
+    while time.perf_counter() < t_end:
+        run_preroll()
+        run_timed()
         torch.cuda.synchronize(dev)
 
-    if dist is not None:
-        dist.barrier()
-    torch.cuda.synchronize(dev)
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
-    ev0.record(stream)
-    if graph is not None:
-        graph.replay()
-    else:
-        for k in range(args.steps):
-            step(k, st_handle)
-    ev1.record(stream)
-    torch.cuda.synchronize(dev)
-    if dist is not None:
-        dist.barrier()
-    ms = ev0.elapsed_time(ev1)
+    def one_region():
+        ctx.barrier()
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        run_preroll()  # untimed, enqueued before ev0 (no host gap before the timed region)
+        ev0.record(stream)
+        run_timed()
+        ev1.record(stream)
+        torch.cuda.synchronize(dev)
+        return ev0.elapsed_time(ev1)
+
+    ms_max = ctx.max_over_ranks([one_region()])[0]
+    # repeat the identical region for a spread (median / p10 / p90 of per-step times)
+    reps = ctx.max_over_ranks([one_region() for _ in range(args.reps)])
     sampler.stop()
-    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if dist is not None:
-        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
-    ms_max = float(ms_t.item())
+
+    # eager launches (no graph): host launch overhead included
+    eager_ms = None
+    if args.mode == "graph":
+        ctx.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        for k in range(-R, 0):
+            step(k, st_handle)
+        e0.record(stream)
+        for k in range(K):
+            step(k, st_handle)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        eager_ms = ctx.max_over_ranks([e0.elapsed_time(e1)])[0] / K
 
     # end-to-end through the public C-ABI host-buffer entry point (pinned host I/O)
-    e2e_steps = args.e2e_steps or max(20, min(args.steps, 400))
-    # page-locked host buffers from the library allocator (ts_host_alloc)
+    e2e_steps = args.e2e_steps or max(20, min(K, 400))
     hp = tsb.host_empty((B, E, C, C))
     hp.copy_(pots[0].cpu())
     hm = tsb.host_empty((B, E, C, C))
@@ -376,9 +486,7 @@ def main():
     hws = tsb.Workspace(dev)
     for _ in range(3):
         tsb.marginals_host(hp, hm, hl, hf, device=dev, ws=hws)
-    torch.cuda.synchronize(dev)
-    if dist is not None:
-        dist.barrier()
+    ctx.barrier()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
@@ -386,44 +494,54 @@ def main():
         tsb.marginals_host(hp, hm, hl, hf, device=dev, ws=hws)
     e1.record(stream)
     torch.cuda.synchronize(dev)
-    e_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
-    if dist is not None:
-        dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
-    e2e_value = world * e2e_steps * cfg.tokens / (float(e_ms.item()) / 1e3)
+    e_ms = ctx.max_over_ranks([e0.elapsed_time(e1)])[0]
+    e2e_value = world * e2e_steps * cfg.tokens / (e_ms / 1e3)
+
+    side = side_configs(ctx, args) if args.side else {}
 
     if rank == 0:
-        value = world * args.steps * cfg.tokens / (ms_max / 1e3)
+        value = world * K * cfg.tokens / (ms_max / 1e3)
         peak, peak_src = load_peaks()
         alg_bytes = 8 * B * E * C * C  # read l + write mu, per launch
-        # the step is one launch of a fused kernel for the short-chain plans (cfg2): its
-        # average launch duration is the timed region / launches
-        launch_s = (ms / 1e3) / (args.steps * launches_per_step) if launches_per_step == 1 \
-            else None
+        # one fused launch per step for the short-chain plans (cfg2): the kernel's average
+        # launch duration = this rank's timed region / launches
+        launch_s = (ms_max / 1e3) / (K * launches_per_step) if launches_per_step == 1 else None
         achieved = (alg_bytes / launch_s / 1e9) if launch_s else None
+        traffic, traffic_src = load_traffic(kernel, cfg.no)
+        per_step = [x / K for x in reps]
+        touched = min(R, K) * set_bytes
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+            "steps": K, "warmup": args.warmup, "ms_per_step": ms_max / K,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (tsgen seeded dyadic potentials, DESIGN.md §3)",
-            "config": {"workload": f"cfg{cfg.no}: {cfg.label}", "B": B, "N": N, "C": C,
-                       "global_batch": B * world, "seq_len": N,
-                       "parallelism": f"batch-sharded dp{world} (B={B} per GPU, no collective)",
-                       "l2": f"inputs rotate over {R} buffer sets ({R * set_bytes / 1e6:.0f} MB > "
-                             f"{l2 / 1e6:.0f} MB L2)",
-                       "launch": "CUDA graph of K ts_marginals calls" if graph else "eager"},
+            "config": cfg_dict(
+                cfg, world, f"batch-sharded dp{world} (B={B} per GPU, no collective)",
+                l2=(f"cold: {R} rotating input/output sets of {set_bytes / 1e6:.2f} MB "
+                    f"({R * set_bytes / 1e6:.0f} MB > 2x {l2 / 1e6:.0f} MB L2); the timed "
+                    f"{K} calls touch {touched / 1e6:.0f} MB and are preceded by an untimed "
+                    f"graph of the {R} calls before them in the rotation, so every timed "
+                    f"call's buffers were last used {R} calls ({R * set_bytes / 1e6:.0f} MB) "
+                    "earlier"),
+                launch="CUDA graph of K ts_marginals calls" if timed else "eager"),
+            "distribution": {"reps": len(per_step), "ms_per_step_median": statistics.median(per_step),
+                             "ms_per_step_p10": pctl(per_step, 0.1),
+                             "ms_per_step_p90": pctl(per_step, 0.9),
+                             "eager_ms_per_step": eager_ms},
             "roofline": {"bound": "hbm", "kernel": kernel,
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None,
-                         "traffic": load_traffic(kernel, cfg.no),
+                         "traffic": traffic, "traffic_source": traffic_src,
                          "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src,
                          "launch_s": launch_s},
             "e2e": {"value": e2e_value, "unit": UNIT,
                     "h2d_bytes_per_step": B * E * C * C * 4,
                     "d2h_bytes_per_step": B * E * C * C * 4 + 8 * B,
-                    "api": "ts_marginals_host (ts_host_alloc page-locked host buffers; H2D, kernels, "
-                           "D2H inside every call)"},
-            "gpu_launches": args.steps * launches_per_step,
+                    "api": "ts_marginals_host (ts_host_alloc page-locked host buffers; H2D, "
+                           "kernels, D2H inside every call)"},
+            "gpu_launches": K * launches_per_step,
             "clocks": sampler.summary(),
+            "side": side,
             "paper_context": {"value": 390000, "unit": UNIT,
                               "hw": "K80 (Google Colab), PAPER.md Table 1 P:41/P:54",
                               "note": "context only, not the target"},
@@ -431,10 +549,106 @@ def main():
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = oracle_baseline(cfg)
         print(json.dumps(line), flush=True)
-    if dist is not None:
-        dist.barrier()
-        dist.destroy_process_group()
+    ctx.close()
     return 0
+
+
+def run_time_sharded(args):
+    """Side mode (not the driver's line): cfg5-style long chains split in TIME across the
+    ranks (DESIGN.md §6): each rank generates its edge range in place, runs the local scan
+    summary, one NCCL all_gather_into_tensor of the C x C summaries, then the combine and its
+    local sweeps + marginals.  Total work is fixed as N grows ("scaling": "strong").  Time =
+    max over ranks of CUDA-event time around K steps (summary + all-gather + finish)."""
+    import paper_2002_00876_b200 as tsb
+    import tsgen
+    from paper_2002_00876_b200 import dist as tdist
+
+    ctx = Ctx()
+    torch = ctx.torch
+    cfg = tsgen.CONFIGS[args.config]
+    B, N, C, E = cfg.B, cfg.N, cfg.C, cfg.E
+    begin, count = tdist.shard_edges(E, ctx.world, ctx.rank)
+    local = torch.empty((B, count, C, C), dtype=torch.float32, device=ctx.dev)
+    tsgen.fill_torch(local, cfg.seed, cfg.quantum, t_begin=begin, E_global=E)
+    seg = tsb.Segment(local, begin, N)
+
+    def step():
+        summ = seg.summary()
+        gathered = tdist._all_gather(summ, None) if ctx.dist is not None else summ[None]
+        return seg.finish(gathered, ctx.rank, ctx.world, True)
+
+    for _ in range(args.warmup):
+        _, logz, flags = step()
+    torch.cuda.synchronize(ctx.dev)
+    assert int(flags.abs().sum()) == 0
+    ctx.barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(ctx.local_rank).start()
+    ev0.record()
+    for _ in range(args.steps):
+        step()
+    ev1.record()
+    torch.cuda.synchronize(ctx.dev)
+    sampler.stop()
+    ms = ctx.max_over_ranks([ev0.elapsed_time(ev1)])[0] / args.steps
+    if ctx.rank == 0:
+        peak, peak_src = load_peaks()
+        alg = 8 * B * E * C * C
+        line = {"metric": f"tokens/sec linear-chain logZ+marginals time-sharded (cfg{cfg.no}: "
+                          f"B={B},N={N},C={C})", "value": B * N / (ms / 1e3), "unit": UNIT,
+                "n_gpus": ctx.world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic (tsgen, generated in place per rank)",
+                "config": {"workload": f"cfg{cfg.no}: {cfg.label}",
+                           "parallelism": f"time-sharded over {ctx.world} GPU(s), one NCCL "
+                                          "all_gather of C x C segment summaries per step",
+                           "l2": f"inputs {alg / 2 / 1e9:.1f} GB >> L2"},
+                "roofline": {"bound": "hbm", "achieved": alg / (ms / 1e3) / 1e9 / ctx.world,
+                             "peak": peak, "unit": "GB/s (per GPU)",
+                             "frac": alg / (ms / 1e3) / 1e9 / ctx.world / peak,
+                             "peak_source": peak_src},
+                "clocks": sampler.summary()}
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    return 0
+
+
+def parse(argv):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=50)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--mode", default="graph", choices=["graph", "eager"])
+    ap.add_argument("--sets", type=int, default=0, help="rotating buffer sets (0 = auto > 2x L2)")
+    ap.add_argument("--reps", type=int, default=5, help="repeats of the timed region (spread)")
+    ap.add_argument("--side", type=lambda s: [int(x) for x in s.split(",") if x], default=[3, 4, 5],
+                    help="side configs measured into the same line ('' = none)")
+    ap.add_argument("--side-reps", type=int, default=10)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=0)
+    ap.add_argument("--time-shard", action="store_true",
+                    help="side mode: time-sharded long chains (use with --config 5)")
+    ap.add_argument("--tiny-mode", type=int, default=-1,
+                    help="debug: cfg2 kernel variant (ts_set_tiny: 1 default, 0 general kernel)")
+    args = ap.parse_args(argv)
+    args.warmup = max(args.warmup, 3)
+    return args
+
+
+def main(argv=None):
+    argv = sys.argv[1:] if argv is None else argv
+    args = parse(argv)
+    rc = maybe_spawn(argv, args.gpus)
+    if rc is not None:
+        return rc
+    if args.impl == "reference":
+        return run_reference(args)
+    if args.time_shard:
+        return run_time_sharded(args)
+    return run_ours(args)
 
 
 if __name__ == "__main__":

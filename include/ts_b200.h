@@ -284,8 +284,9 @@ TS_API void  ts_host_free(void *p);
  * Step 1: ts_segment_summary writes this segment's C x C transfer matrix per sequence
  *         (the semiring product of its edges) into `summary` (16-byte aligned),
  *         laid out as ts_segment_summary_bytes(local) bytes: [B][C][C] fp32 log2-domain
- *         values relative to per-row fp64 natural-log offsets, followed by [B][C] fp64
- *         offsets.  The workspace (size: ts_workspace_bytes(local, TS_OP_SEGMENT, s)) holds
+ *         values relative to per-row fp64 natural-log offsets (this section padded to a
+ *         multiple of 4 floats), followed by [B][C] fp64 offsets (padded to an even count),
+ *         so the size is a multiple of 16 bytes and every gathered slice stays aligned.  The workspace (size: ts_workspace_bytes(local, TS_OP_SEGMENT, s)) holds
  *         the local scan tree and MUST be passed unchanged to ts_segment_finish.
  * Step 2: the caller all-gathers the summaries of all `world` segments, in rank order,
  *         into all_summaries ([world] x ts_segment_summary_bytes) — e.g. NCCL

@@ -319,7 +319,8 @@ class Segment:
 
     def summary(self) -> torch.Tensor:
         """This segment's C x C transfer matrices (the local semiring product) as
-        float32 words [B*C*C + 2*B*C] (fp64 row offsets packed after the matrices)."""
+        float32 words (ts_segment_summary_bytes / 4: the [B, C, C] matrices padded to 16 bytes,
+        then the [B, C] fp64 row offsets, include/ts_b200.h)."""
         L = _lib.load()
         out = torch.empty(self.nbytes // 4, dtype=torch.float32, device=self.pot.device)
         _lib.check(L.ts_segment_summary(ctypes.byref(self.ch), self.edge_begin, self.n_global,

@@ -488,14 +488,20 @@ struct HostKey {
   void* ws;
   size_t ws_bytes;
   int64_t plan_chunk;
-  int meet, small_cluster;
+  int64_t knobs;  // every kernel-selection knob (knob_word): a toggle never replays a stale graph
   bool operator==(const HostKey& o) const {
     return B == o.B && N == o.N && C == o.C && pot == o.pot && lengths == o.lengths && s == o.s &&
            marg == o.marg && logz == o.logz && flags == o.flags && ws == o.ws &&
-           ws_bytes == o.ws_bytes && plan_chunk == o.plan_chunk && meet == o.meet &&
-           small_cluster == o.small_cluster;
+           ws_bytes == o.ws_bytes && plan_chunk == o.plan_chunk && knobs == o.knobs;
   }
 };
+
+// All debug knobs that change which kernels a call enqueues, packed into one key word.
+int64_t knob_word() {
+  return (int64_t)g_meet.load() | ((int64_t)g_small_cluster.load() << 1) |
+         ((int64_t)tsb::get_tc_summary() << 4) | ((int64_t)g_tiny.load() << 8) |
+         ((int64_t)(g_vsplit.load() + 1) << 9) | ((int64_t)(tsb::g_wide_ring != 0) << 14);
+}
 
 struct HostGraph {
   HostKey key;
@@ -515,6 +521,11 @@ struct HostPipe {
   // staging buffers; ev_in[p] = copy-in done, ev_done[p] = the call that used buffer p done
   cudaStream_t cin;
   cudaEvent_t ev_in[2], ev_done[2];
+  // the previous call (any path) and its stream: a call on another stream orders after it,
+  // since all calls share the device staging buffers and the inner workspace
+  cudaEvent_t ev_last;
+  cudaStream_t last_st = nullptr;
+  bool has_last = false;
   int parity = 0;
   bool primed[2] = {false, false};
   int64_t sig[5] = {0, 0, 0, 0, 0};  // (B, N, C, ws, semiring) of the last pipelined call
@@ -556,6 +567,7 @@ HostPipe* host_pipe() {
   if (!pipes[dev]) {
     HostPipe* p = new HostPipe;
     bool ok = cudaEventCreateWithFlags(&p->fork, cudaEventDisableTiming) == cudaSuccess &&
+              cudaEventCreateWithFlags(&p->ev_last, cudaEventDisableTiming) == cudaSuccess &&
               cudaStreamCreateWithFlags(&p->cap, cudaStreamNonBlocking) == cudaSuccess &&
               cudaStreamCreateWithFlags(&p->cin, cudaStreamNonBlocking) == cudaSuccess;
     for (int k = 0; k < 2 && ok; ++k)
@@ -1197,8 +1209,7 @@ static ts_status host_pipelined(HostPipe* hp, const ts_chain* hc, ts_semiring s,
   ts_chain dc{B, N, C, nel ? d_pot : nullptr, hc->lengths ? d_len : nullptr};
   // scan + copy-back: graph replay for a repeated binding (parity is part of the key)
   HostKey key{hc->B, hc->N, hc->C, hc->pot, hc->lengths, (int)s + 8 * (p + 1), host_marg,
-              host_logz, host_flags, ws, ws_bytes, g_plan_chunk.load(), g_meet.load(),
-              g_small_cluster.load() * 16 + tsb::get_tc_summary()};
+              host_logz, host_flags, ws, ws_bytes, g_plan_chunk.load(), knob_word()};
   HostGraph* g = hp->find(key);
   ts_status r = TS_OK;
   if (g && g->exec) {
@@ -1237,18 +1248,10 @@ static ts_status host_pipelined(HostPipe* hp, const ts_chain* hc, ts_semiring s,
   return TS_OK;
 }
 
-TS_API ts_status ts_marginals_host(const ts_chain* hc, ts_semiring s, float* host_marg,
-                                   float* host_logz, uint32_t* host_flags, void* ws,
-                                   size_t ws_bytes, void* stream) {
-  if (!chain_ok(hc) || !host_marg || !host_logz) return TS_E_INVALID;
-  if (s != TS_LOG && s != TS_MAX) return TS_E_INVALID;
-  if (!device_ok()) return TS_E_UNSUPPORTED;
-  const size_t need = ts_workspace_bytes(hc, TS_OP_MARG_HOST, s);
-  if (ws_bytes < need || !ws || !aligned(ws, kAlign)) return TS_E_WORKSPACE;
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  HostPipe* hp = host_pipe();
-  if (!hp) return TS_E_CUDA;
-  std::lock_guard<std::mutex> lock(hp->mu);
+// ts_marginals_host body, under hp->mu, after the cross-stream ordering.
+ts_status marginals_host_locked(HostPipe* hp, const ts_chain* hc, ts_semiring s,
+                                float* host_marg, float* host_logz, uint32_t* host_flags,
+                                void* ws, size_t ws_bytes, cudaStream_t st) {
   if (g_host_pipeline.load() && host_chunks(hc->B, (hc->N - 1) * hc->C * hc->C) == 1)
     return host_pipelined(hp, hc, s, host_marg, host_logz, host_flags, ws, ws_bytes, st);
   // a stream-ordered call: the next pipelined call must order its copy-in after it again
@@ -1256,7 +1259,7 @@ TS_API ts_status ts_marginals_host(const ts_chain* hc, ts_semiring s, float* hos
   // Replay path: the same I/O binding seen before -> one graph launch (all copies and
   // kernels of the call are nodes of the instantiated graph; nothing is skipped).
   HostKey key{hc->B, hc->N, hc->C, hc->pot, hc->lengths, (int)s, host_marg, host_logz,
-              host_flags, ws, ws_bytes, g_plan_chunk.load(), g_meet.load(), g_small_cluster.load() * 16 + tsb::get_tc_summary()};
+              host_flags, ws, ws_bytes, g_plan_chunk.load(), knob_word()};
   HostGraph* g = hp->find(key);
   if (g && g->exec) {
     cudaError_t e = cudaGraphLaunch(g->exec, st);
@@ -1293,6 +1296,33 @@ TS_API ts_status ts_marginals_host(const ts_chain* hc, ts_semiring s, float* hos
   return TS_OK;
 }
 
+TS_API ts_status ts_marginals_host(const ts_chain* hc, ts_semiring s, float* host_marg,
+                                   float* host_logz, uint32_t* host_flags, void* ws,
+                                   size_t ws_bytes, void* stream) {
+  if (!chain_ok(hc) || !host_marg || !host_logz) return TS_E_INVALID;
+  if (s != TS_LOG && s != TS_MAX) return TS_E_INVALID;
+  if (!device_ok()) return TS_E_UNSUPPORTED;
+  const size_t need = ts_workspace_bytes(hc, TS_OP_MARG_HOST, s);
+  if (ws_bytes < need || !ws || !aligned(ws, kAlign)) return TS_E_WORKSPACE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  HostPipe* hp = host_pipe();
+  if (!hp) return TS_E_CUDA;
+  std::lock_guard<std::mutex> lock(hp->mu);
+  cudaError_t e;
+  // every call shares the device staging buffers, d_marg/d_logz/d_flags and the inner
+  // workspace: a call on a different stream than the previous one first waits for it
+  if (hp->has_last && hp->last_st != st &&
+      (e = cudaStreamWaitEvent(st, hp->ev_last, 0)) != cudaSuccess)
+    return cuda_status(e);
+  const ts_status r =
+      marginals_host_locked(hp, hc, s, host_marg, host_logz, host_flags, ws, ws_bytes, st);
+  if (r != TS_OK) return r;
+  if ((e = cudaEventRecord(hp->ev_last, st)) != cudaSuccess) return cuda_status(e);
+  hp->last_st = st;
+  hp->has_last = true;
+  return TS_OK;
+}
+
 TS_API void ts_set_host_graphs(int on) { g_host_graphs.store(on ? 1 : 0); }
 TS_API void ts_set_host_pipeline(int on) { g_host_pipeline.store(on ? 1 : 0); }
 
@@ -1318,8 +1348,7 @@ TS_API void ts_host_free(void* p) {
 
 TS_API size_t ts_segment_summary_bytes(const ts_chain* local) {
   if (!chain_ok(local)) return 0;
-  return (size_t)(local->B * local->C * local->C) * sizeof(float) +
-         (size_t)(local->B * local->C) * sizeof(double);
+  return (size_t)seg_total_floats(local->B, local->C) * sizeof(float);
 }
 
 TS_API ts_status ts_segment_summary(const ts_chain* local, int64_t edge_begin, int64_t n_global,

@@ -8,9 +8,26 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #include "ts_b200.h"
 
 namespace tsb {
+
+// One-time opt-in of kernel `kern` to `bytes` of dynamic shared memory, per DEVICE: the
+// attribute is device state, so bit d of `mask` (one mask per kernel instantiation) records
+// that device d has it.  Devices >= 64 (none exist on one node) re-apply it every launch.
+template <typename K>
+inline cudaError_t smem_optin_once(K kern, std::atomic<uint64_t>& mask, int bytes) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const uint64_t bit = (dev >= 0 && dev < 64) ? (1ull << dev) : 0;
+  if (bit && (mask.load(std::memory_order_acquire) & bit)) return cudaSuccess;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess && bit) mask.fetch_or(bit, std::memory_order_release);
+  return e;
+}
 
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr double kLn2 = 0.69314718055994530942;

@@ -529,7 +529,7 @@ __global__ void __launch_bounds__(kNT, 2) meet64_kernel(MeetArgs a) {
   }
 }
 
-std::atomic<int> g_meet_attr{0};
+std::atomic<uint64_t> g_meet_attr{0};
 }  // namespace
 
 bool meet_ok(int64_t C, const float* pot, const float* marg) {
@@ -539,15 +539,8 @@ bool meet_ok(int64_t C, const float* pot, const float* marg) {
 
 cudaError_t launch_meet(const MeetArgs& a, int64_t C, cudaStream_t st) {
   if (C != kC) return cudaErrorInvalidValue;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  const int bit = 1 << (dev & 31);
-  if (!(g_meet_attr.load() & bit)) {
-    cudaError_t e = cudaFuncSetAttribute(meet64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)sizeof(MeetSmem));
-    if (e != cudaSuccess) return e;
-    g_meet_attr.fetch_or(bit);
-  }
+  cudaError_t e = smem_optin_once(meet64_kernel, g_meet_attr, (int)sizeof(MeetSmem));
+  if (e != cudaSuccess) return e;
   meet64_kernel<<<(unsigned)a.B, kNT, sizeof(MeetSmem), st>>>(a);
   return cudaGetLastError();
 }

@@ -499,17 +499,11 @@ int bwd_stages(int C, bool vec4) {
   int S = (int)(budget / tile);
   return S < 2 ? 2 : (S > 8 ? 8 : S);
 }
-std::atomic<uint64_t> g_attr_fwd{0}, g_attr_bwd{0};
+std::atomic<uint64_t> g_attr_fwd[64], g_attr_bwd[64];  // per-device masks, one per kernel id
 
 template <typename K>
-cudaError_t set_smem_once(K kern, std::atomic<uint64_t>& mask, int bit) {
-  int dev = 0;
-  cudaGetDevice(&dev);
-  const uint64_t m = 1ull << ((dev & 7) * 8 + bit);
-  if (mask.load() & m) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-  if (e == cudaSuccess) mask.fetch_or(m);
-  return e;
+cudaError_t set_smem_once(K kern, std::atomic<uint64_t>* masks, int bit) {
+  return smem_optin_once(kern, masks[bit], 220 * 1024);
 }
 }  // namespace
 

@@ -503,16 +503,10 @@ __global__ void __launch_bounds__(kNT2) bwd2_kernel(SweepArgs a, int S) {
 // host side
 // ====================================================================================
 namespace {
-std::atomic<uint64_t> g_attr2{0};
+std::atomic<uint64_t> g_attr2[64];  // one per-device mask per kernel (`bit` = kernel id)
 template <typename K>
 cudaError_t set_smem2(K kern, int bit) {
-  int dev = 0;
-  cudaGetDevice(&dev);
-  const uint64_t m = 1ull << ((dev & 7) * 8 + bit);
-  if (g_attr2.load() & m) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-  if (e == cudaSuccess) g_attr2.fetch_or(m);
-  return e;
+  return smem_optin_once(kern, g_attr2[bit], 220 * 1024);
 }
 template <int C>
 size_t fwd2_smem(int S) {

@@ -456,12 +456,10 @@ cudaError_t launch_fb_wide(const SemiArgs& a, cudaStream_t st) {
   const dim3 grid((unsigned)a.B, a.marg ? 2u : 1u);
   if (a.C % 4 == 0 && g_wide_ring) {
     const size_t smem = (size_t)kWideRing * 32 * a.C * sizeof(float);
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(fb_wide_ring_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)((size_t)kWideRing * 32 * kWideMaxC * sizeof(float)));
-      attr = true;
-    }
+    static std::atomic<uint64_t> attr{0};
+    cudaError_t ea = smem_optin_once(fb_wide_ring_kernel, attr,
+                                     (int)((size_t)kWideRing * 32 * kWideMaxC * sizeof(float)));
+    if (ea != cudaSuccess) return ea;
     fb_wide_ring_kernel<<<grid, kRingThreads, smem, st>>>(a);
   } else {
     fb_wide_sweep_kernel<<<grid, kWideThreads, 0, st>>>(a);

@@ -118,6 +118,15 @@ __host__ __device__ int64_t level_off(int l, int64_t Ppad);
 size_t scan_mat_smem(int64_t C);
 cudaError_t launch_scan_up(const ScanArgs& a, cudaStream_t st, int* launches);
 cudaError_t launch_scan_down(const ScanArgs& a, cudaStream_t st, int* launches, bool set_root);
+// Segment summary layout (ts_segment_summary_bytes): [B][C][C] fp32, padded to a multiple
+// of 4 floats so the fp64 offsets that follow are 16-byte aligned whatever B*C*C is, then
+// [B][C] fp64 padded to an even count so every gathered slice stays 16-byte aligned.
+__host__ __device__ inline int64_t seg_mat_floats(int64_t B, int64_t C) {
+  return (B * C * C + 3) & ~int64_t(3);
+}
+__host__ __device__ inline int64_t seg_total_floats(int64_t B, int64_t C) {
+  return seg_mat_floats(B, C) + 2 * ((B * C + 1) & ~int64_t(1));
+}
 cudaError_t launch_segment_export(const ScanArgs& a, float* summ, cudaStream_t st);
 cudaError_t launch_segment_combine(const ScanArgs& a, const float* all_summ, int rank, int world,
                                    bool write_root, cudaStream_t st);

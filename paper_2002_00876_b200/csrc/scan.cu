@@ -648,14 +648,15 @@ __global__ void tree_leaves_kernel(ScanArgs a) {
 // ====================================================================================
 // Time sharding: export the local root as this segment's summary; combine
 // all gathered segment summaries into the local root vectors and the global logZ.
-// Summary layout: [B][C][C] fp32 log2 values, then [B][C] fp64 natural row offsets.
+// Summary layout: [B][C][C] fp32 log2 values, then [B][C] fp64 natural row offsets, each
+// section padded to 16 bytes (seg_mat_floats / seg_total_floats, kernels.cuh).
 // ====================================================================================
 __global__ void __launch_bounds__(kScanThreads) segment_export_kernel(ScanArgs a, float* summ) {
   const int C = (int)a.C, CC = C * C;
   const int64_t b = blockIdx.x;
   const int64_t nr = b * a.nodes + level_off(a.H, a.Ppad);
   float* S = summ + b * CC;
-  double* O = reinterpret_cast<double*>(summ + a.B * CC) + b * C;
+  double* O = reinterpret_cast<double*>(summ + seg_mat_floats(a.B, C)) + b * C;
   const bool id = a.ident[nr];
   // a NaN / +inf anywhere in this segment poisons its summary so every rank sees it
   const bool bad = a.wflags && (a.wflags[b] & WF_NONFINITE);
@@ -678,10 +679,11 @@ __global__ void __launch_bounds__(kScanThreads) segment_combine_kernel(ScanArgs 
   float* vb = va + C4;         // output vector
   float* scratch = vb + C4;
   double* vo = reinterpret_cast<double*>(scratch + 4 * C4 + 32);  // [2]
-  const size_t seg_floats = (size_t)B * CC + (size_t)B * C * 2;   // fp64 offsets = 2 floats
+  const size_t seg_floats = (size_t)seg_total_floats(B, C);  // one rank's slice
+  const size_t mat_floats = (size_t)seg_mat_floats(B, C);
   auto segS = [&](int g) { return all_summ + (size_t)g * seg_floats + b * CC; };
   auto segO = [&](int g) {
-    return reinterpret_cast<const double*>(all_summ + (size_t)g * seg_floats + B * CC) + b * C;
+    return reinterpret_cast<const double*>(all_summ + (size_t)g * seg_floats + mat_floats) + b * C;
   };
   const int64_t nr = b * a.nodes + level_off(a.H, a.Ppad);
   // a poisoned (NaN) summary anywhere -> NONFINITE on every rank, local sweeps zeroed
@@ -764,16 +766,10 @@ __global__ void __launch_bounds__(kScanThreads) segment_combine_kernel(ScanArgs 
 // host side
 // ====================================================================================
 namespace {
-std::atomic<uint64_t> g_attr_scan{0};
+std::atomic<uint64_t> g_attr_scan[64];  // one per-device mask per kernel (`bit` = kernel id)
 template <typename K>
 cudaError_t set_smem(K kern, int bit) {
-  int dev = 0;
-  cudaGetDevice(&dev);
-  const uint64_t m = 1ull << ((dev & 3) * 16 + bit);
-  if (g_attr_scan.load() & m) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024);
-  if (e == cudaSuccess) g_attr_scan.fetch_or(m);
-  return e;
+  return smem_optin_once(kern, g_attr_scan[bit], 225 * 1024);
 }
 template <int RB>
 size_t fast_smem(int C) {

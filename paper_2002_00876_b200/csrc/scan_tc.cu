@@ -381,18 +381,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) summary_tc_kernel(ScanArgs a) {
 
 namespace {
 std::atomic<int> g_tc_summary{3};  // 0 = SIMT summaries, 1 = 1xTF32, 3 = 3xTF32 (default)
-std::atomic<uint64_t> g_tc_attr2{0};
 template <int NP, int CF>
 cudaError_t launch_np(const ScanArgs& a, cudaStream_t st) {
-  int dev = 0;
-  cudaGetDevice(&dev);
-  const uint64_t bit = 1ull << ((dev & 15) * 4 + (NP == 3 ? 1 : 0) + (CF ? 2 : 0));
-  if (!(g_tc_attr2.load() & bit)) {
-    cudaError_t e = cudaFuncSetAttribute(summary_tc_kernel<NP, CF>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem);
-    if (e != cudaSuccess) return e;
-    g_tc_attr2.fetch_or(bit);
-  }
+  static std::atomic<uint64_t> attr{0};  // per instantiation, one bit per device
+  cudaError_t e = smem_optin_once(summary_tc_kernel<NP, CF>, attr, kTcSmem);
+  if (e != cudaSuccess) return e;
   summary_tc_kernel<NP, CF><<<(unsigned)(a.B * a.Ppad), kTcThreads, kTcSmem, st>>>(a);
   return cudaGetLastError();
 }

@@ -260,14 +260,12 @@ cudaError_t launch_semimarkov(const SemiArgs& a0, cudaStream_t st) {
   const size_t smem = (size_t)2 * R * GS * sizeof(float) + (size_t)2 * R * sizeof(double) +
                       16 * sizeof(float) + 16 + (size_t)2 * GS * sizeof(float) +
                       (a.staged ? stage_bytes : 0);
-  static bool attr = false;
-  if (!attr) {
-    const int mx = (int)((size_t)2 * 17 * 256 * sizeof(float) + 2 * 17 * sizeof(double) + 64 +
-                         2 * 256 * sizeof(float) + kSemiStageBytes);
-    cudaFuncSetAttribute(semimarkov_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(semimarkov_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr128{0}, attr256{0};
+  const int mx = (int)((size_t)2 * 17 * 256 * sizeof(float) + 2 * 17 * sizeof(double) + 64 +
+                       2 * 256 * sizeof(float) + kSemiStageBytes);
+  cudaError_t ea = GS == 128 ? smem_optin_once(semimarkov_kernel<128>, attr128, mx)
+                             : smem_optin_once(semimarkov_kernel<256>, attr256, mx);
+  if (ea != cudaSuccess) return ea;
   if (GS == 128)
     semimarkov_kernel<128><<<(unsigned)a.B, 256, smem, st>>>(a);
   else

@@ -425,3 +425,55 @@ def test_cluster_dsmem_variant(dev, G):
         assert_log_parity(tsgen.large_offset_potentials(2, 30, 20, seed=2), None, dev)
     finally:
         tsb.set_small_cluster(0)
+
+
+def test_host_calls_switching_streams(dev):
+    """ts_marginals_host calls alternating between two torch streams without synchronising
+    (same hidden workspace and device staging): each call orders after the previous one on
+    the other stream, so every result is right."""
+    B, N, C = 32, 25, 20
+    streams = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
+    outs = []
+    for k in range(8):
+        pot_np = tsgen.potentials(B, N, C, seed=1300 + k)
+        pot = torch.from_numpy(pot_np).pin_memory()
+        marg = torch.empty_like(pot).pin_memory()
+        logz = torch.empty(B, dtype=torch.float32).pin_memory()
+        flags = torch.empty(B, dtype=torch.int32).pin_memory()
+        with torch.cuda.stream(streams[k % 2]):
+            tsb.marginals_host(pot, marg, logz, flags, device=dev)
+        outs.append((pot_np, marg, logz, flags))
+    torch.cuda.synchronize()
+    for pot_np, marg, logz, flags in outs:
+        lz_ref, mg_ref, fl_ref = oracle.chain_marginals(pot_np)
+        check_logz(logz.numpy(), lz_ref)
+        check_marg(marg.numpy(), mg_ref)
+        np.testing.assert_array_equal(flags.numpy(), fl_ref)
+
+
+def test_host_graph_key_covers_kernel_knobs(dev):
+    """A repeated host binding replays its graph, but toggling a kernel-selection knob
+    (ts_set_tiny) must re-enqueue with the newly selected kernel, not replay the old one."""
+    B, N, C = 32, 25, 20
+    pot_np = tsgen.potentials(B, N, C, seed=1400)
+    pot = torch.from_numpy(pot_np).pin_memory()
+    marg = torch.empty_like(pot).pin_memory()
+    logz = torch.empty(B, dtype=torch.float32).pin_memory()
+    flags = torch.empty(B, dtype=torch.int32).pin_memory()
+    lz_ref, mg_ref, _ = oracle.chain_marginals(pot_np)
+    try:
+        tsb.set_host_pipeline(False)
+        for _ in range(3):  # eager, capture, replay
+            tsb.marginals_host(pot, marg, logz, flags, device=dev)
+        torch.cuda.synchronize()
+        k_tiny = tsb.last_kernel()
+        tsb.set_tiny(0)
+        tsb.marginals_host(pot, marg, logz, flags, device=dev)
+        torch.cuda.synchronize()
+        k_small = tsb.last_kernel()
+        assert k_tiny != k_small, (k_tiny, k_small)
+        check_logz(logz.numpy(), lz_ref)
+        check_marg(marg.numpy(), mg_ref)
+    finally:
+        tsb.set_tiny(1)
+        tsb.set_host_pipeline(True)

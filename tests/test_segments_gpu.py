@@ -34,7 +34,10 @@ def virtual_segments(pot_np, G, dev, want_marg=True):
 
 
 @pytest.mark.parametrize("B,N,C,G", [(4, 257, 64, 2), (2, 1001, 128, 8), (3, 120, 20, 4),
-                                     (2, 50, 3, 8), (2, 9, 37, 8)])
+                                     (2, 50, 3, 8), (2, 9, 37, 8),
+                                     # B*C*C odd: the fp64 offsets follow a padded matrix
+                                     # section (was a misaligned-address fault)
+                                     (1, 40, 5, 2), (1, 60, 37, 4), (3, 31, 5, 3)])
 def test_virtual_segments_match_unsharded(dev, B, N, C, G):
     pot = tsgen.potentials(B, N, C, seed=31 + G)
     lz_ref, mg_ref, fl_ref = oracle.chain_marginals(pot, threads=8)

@@ -256,3 +256,15 @@ def fill_torch(t, cfg_or_seed, s: int | None = None, t_begin: int = 0, E_global:
     fill_device(t.data_ptr(), B, E_local, C, seed, s, t_begin, E_global,
                 torch.cuda.current_stream(t.device).cuda_stream)
     return t
+
+
+def fill_torch_batch(t, cfg: Config, b_begin: int):
+    """Fill sequences [b_begin, b_begin + t.shape[0]) of a config's batch (global indices:
+    the rank's slice of a batch-sharded input equals that slice of the unsharded one).  The
+    flat index ((b·E + t)·C + i)·C + j is contiguous in b, so the slice is one [1, nb·E]
+    'chain' starting at edge b_begin·E of a B·E-edge index space (same values, same s)."""
+    nb, E, C, _ = t.shape
+    assert E == cfg.E and C == cfg.C and 0 <= b_begin and b_begin + nb <= cfg.B
+    fill_torch(t.view(1, nb * E, C, C), cfg.seed, cfg.quantum, t_begin=b_begin * E,
+               E_global=cfg.B * E)
+    return t
