@@ -259,12 +259,17 @@ class Ctx:
             self.dist.destroy_process_group()
 
 
-def timed_calls(ctx, call, reps: int, warmup: int = 3):
+def timed_calls(ctx, call, reps: int, warmup: int = 3, settle_s: float = 0.4):
     """Per-call CUDA-event times (ms) of `call()` on the current stream, each call bracketed
-    by events; returns the per-rep max over ranks."""
+    by events, after `warmup` calls and >= settle_s of untimed calls (clocks settle under
+    the load and the nvidia-smi sampler sees it); returns the per-rep max over ranks."""
     torch = ctx.torch
     for _ in range(warmup):
         call()
+    t_end = time.perf_counter() + settle_s
+    while time.perf_counter() < t_end:
+        call()
+        torch.cuda.synchronize(ctx.dev)
     ctx.barrier()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(reps)]
@@ -338,6 +343,7 @@ def side_configs(ctx, args):
             call()
             kernel, launches = tsb.last_kernel(), tsb.last_launch_count()
         sampler.start()
+        time.sleep(0.2)  # nvidia-smi start-up
         ms = timed_calls(ctx, call, reps=args.side_reps)
         sampler.stop()
         med = statistics.median(ms)
@@ -524,7 +530,8 @@ def run_ours(args):
                     f"call's buffers were last used {R} calls ({R * set_bytes / 1e6:.0f} MB) "
                     "earlier"),
                 launch="CUDA graph of K ts_marginals calls" if timed else "eager"),
-            "distribution": {"reps": len(per_step), "ms_per_step_median": statistics.median(per_step),
+            "distribution": {"reps": len(per_step),
+                             "ms_per_step_median": statistics.median(per_step) if per_step else None,
                              "ms_per_step_p10": pctl(per_step, 0.1),
                              "ms_per_step_p90": pctl(per_step, 0.9),
                              "eager_ms_per_step": eager_ms},
@@ -626,7 +633,7 @@ def parse(argv):
     ap.add_argument("--reps", type=int, default=5, help="repeats of the timed region (spread)")
     ap.add_argument("--side", type=lambda s: [int(x) for x in s.split(",") if x], default=[3, 4, 5],
                     help="side configs measured into the same line ('' = none)")
-    ap.add_argument("--side-reps", type=int, default=10)
+    ap.add_argument("--side-reps", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=0)
     ap.add_argument("--time-shard", action="store_true",

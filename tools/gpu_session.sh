@@ -10,7 +10,7 @@ timeout 1800 python -m pytest tests -m gpu -q -x --timeout=1500 -p no:cacheprovi
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/${T}_smoke.log 2>&1; echo "rc=$?" >> $O/${T}_smoke.log
 timeout 600 python bench.py > $O/${T}_bench.json 2>$O/${T}_bench.err
 timeout 300 python bench.py --impl reference > $O/${T}_ref.json 2>>$O/${T}_bench.err
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv \
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"fb_|meet|summary|tree|fwd|bwd|vit|backtrack|segment" -c 60 --csv \
   --log-file $O/${T}_launches_cfg2.csv python bench.py --steps 20 --warmup 3 --reps 0 --side "" \
   --no-cpu-baseline --e2e-steps 1 > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:fb_tiny -s 10 -c 1 \
