@@ -312,9 +312,14 @@ TS_API ts_status ts_segment_finish(const ts_chain *local, int64_t edge_begin, in
 TS_API void ts_set_plan_chunk(int64_t L);
 TS_API int64_t ts_get_plan_chunk(void);
 
-/* Debug/testing knob (process-global): run short chains with C <= 32 as the chunked scan
- * on a thread-block cluster of G CTAs per sequence exchanging chunk summaries through
- * distributed shared memory (G in {2, 4}; 0 = the default one-CTA-per-sequence kernel). */
+/* Plan knob (process-global) for short log-semiring chains with C % 4 == 0, C <= 28 and
+ * 2G <= N-1 <= 8G: the chunked parallel scan of PAPER.md §6(a) on a thread-block
+ * cluster of G CTAs per sequence — per-CTA chunk summaries (tree of C x C products), one
+ * DSMEM bulk exchange, boundary vectors, local forward/backward sweeps with fused marginals
+ * (fb_cscan.cu).  0 (default) = the one-CTA-per-sequence kernels (fb_tiny measured faster
+ * at cfg2: 6.25 vs 6.8 us/step); -1 = auto (G = 4 if 4B <= #SMs, else 2 if
+ * 2B <= #SMs, else one CTA); 2 or 4 = force that G where the shape fits.  Results agree within the parity tolerances (gated inputs fall back to the
+ * exact one-CTA body inside the same launch). */
 TS_API void ts_set_small_cluster(int G);
 
 /* Debug/testing knob (process-global): 1 (default) runs short log-semiring chains with

@@ -468,7 +468,9 @@ def set_plan_chunk(L: int) -> None:
 
 
 def set_small_cluster(G: int) -> None:
-    """Debug knob: short C<=32 chains on G-CTA clusters (chunked scan over DSMEM); 0 = off."""
+    """Plan knob for short C % 4 == 0, C <= 28 chains: the §6(a) chunked scan on a G-CTA
+    cluster per sequence (fb_cscan.cu).  0 = one CTA per sequence (default), -1 = auto,
+    2 / 4 = force G where the shape fits."""
     _lib.load().ts_set_small_cluster(int(G))
 
 

@@ -15,7 +15,7 @@ using namespace tsb;
 namespace {
 
 std::atomic<int64_t> g_plan_chunk{0};
-std::atomic<int> g_small_cluster{0};
+std::atomic<int> g_small_cluster{0};  // short chains: 0 one CTA (default), -1 auto cluster scan, 2/4 forced G
 std::atomic<int> g_meet{1};
 std::atomic<int> g_tiny{1};    // short chains: 1 = fb_tiny when eligible, 0 = fb_small only
 std::atomic<int> g_vsplit{0};  // Viterbi: -1 one CTA per sequence, 0 auto, G forced cluster size  // meet-in-the-middle marginals kernel for C = 64  // debug: run short C<=32 chains on G-CTA clusters
@@ -78,6 +78,21 @@ struct Plan {
 // Plan selection: the fused small kernel for short chains with C <= 32;
 // otherwise the streaming sweeps, time-chunked with the scan tree when the batch alone
 // cannot fill the GPU (or when the debug knob asks for a chunk length).
+// SM count of the current device (cached per device: the plan is chosen on every call).
+int device_sms() {
+  static std::atomic<int> cache[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  if (dev >= 0 && dev < 64) {
+    const int v = cache[dev].load(std::memory_order_relaxed);
+    if (v > 0) return v;
+  }
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (dev >= 0 && dev < 64) cache[dev].store(sms, std::memory_order_relaxed);
+  return sms;
+}
+
 Plan log_plan(const ts_chain* c) {
   const int64_t knob = g_plan_chunk.load();
   const int64_t E = c->N - 1;
@@ -88,10 +103,7 @@ Plan log_plan(const ts_chain* c) {
       p.kind = PlanKind::Small;
       return p;
     }
-    int sms = 148;
-    int dev = 0;
-    if (cudaGetDevice(&dev) == cudaSuccess)
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int sms = device_sms();
     if (c->B < sms && E >= 64) {
       P = (sms + c->B - 1) / c->B;
       const int64_t cap = (E + 31) / 32;  // chunks of at least 32 edges
@@ -273,11 +285,16 @@ ts_status run_log(const ts_chain* c, float* marg, float* logz, uint32_t* flags, 
   }
   if (p.kind == PlanKind::Small) {
     SmallArgs a{c->pot, c->lengths, c->B, c->N, c->C, marg, logz, flags};
-    const int G = g_small_cluster.load();
+    const int knob = g_small_cluster.load();
+    int G = 0;
+    if (knob < 0)
+      G = g_tiny.load() ? cscan_g(a, device_sms()) : 0;
+    else if (cscan_fits(a, knob))
+      G = knob;
     ts_status r;
-    if (G > 1 && cluster_fits(c->N, c->C, G)) {
-      r = cuda_status(launch_cluster(a, G, st));
-      t_kernel = "fb_cluster_kernel";
+    if (G > 1) {
+      r = cuda_status(launch_cscan(a, G, st));
+      t_kernel = "fb_cscan_kernel";
     } else if (g_tiny.load() && tiny_fits(a)) {
       r = cuda_status(launch_tiny(a, st));
       t_kernel = "fb_tiny_kernel";
@@ -1438,7 +1455,7 @@ TS_API void ts_set_viterbi_split(int G) {
 TS_API void ts_set_plan_chunk(int64_t L) { g_plan_chunk.store(L < 0 ? 0 : L); }
 TS_API int64_t ts_get_plan_chunk(void) { return g_plan_chunk.load(); }
 TS_API void ts_set_small_cluster(int G) {
-  g_small_cluster.store((G == 2 || G == 4) ? G : 0);
+  g_small_cluster.store((G == 2 || G == 4) ? G : (G < 0 ? -1 : 0));
 }
 TS_API void ts_set_tiny(int enable) { g_tiny.store(enable ? 1 : 0); }
 TS_API void ts_set_wide_ring(int enable) { g_wide_ring = enable ? 1 : 0; }

@@ -1,0 +1,467 @@
+// fb_cscan.cu — the chunked parallel scan of PAPER.md §6(a) (Fig. 4)
+// for short chains (C % 4 == 0, C <= 28: the paper's Table 1 setting B=32, N=25, C=20,
+// P:54), one thread-block CLUSTER of G CTAs (G SMs) per sequence.
+//
+// A single CTA per sequence is bounded by one SM's resources: it must ingest all of the
+// sequence's tiles (38 KB at cfg2) through one SM's L2 port, run every exp of the prepass on
+// one SM's MUFU, and walk two serial E-step recursions.  Here CTA r of the cluster owns the
+// contiguous edge chunk [s_r, e_r), s_r = floor(r Eb / G), and
+//
+//  1. bulk-loads (TMA) and preps its L_r tiles exactly as fb_tiny does (tiny.cuh):
+//     EX_t = 2^((l_t - T_t) log2 e) in a row-major and a transposed layout whose spare rows
+//     hold the column sums and the row sums;
+//  2. reduces them to its chunk summary M_r = EX_{s_r} ... EX_{e_r - 1} (the semiring product
+//     of P:310 in the exp-shifted linear form of §6(c), with the chunk's scalar
+//     offset Σ T_t) as C + 1 independent row chains (row i = e_i^T M, row C = 1^T M = the
+//     column sums; the row sums come from the spare lane), L_r vector x matrix steps each,
+//     interleaved R per warp, no block barrier inside;
+//  3. sends M_r to every peer with one bulk copy each (cp.async.bulk shared::cta ->
+//     shared::cluster, completing on the receiver's mbarrier): peers after r receive the
+//     transposed layout (they multiply vectors from the left), peers before r the row-major;
+//  4. forms its boundary vectors alpha_in = 1^T M_0 ... M_{r-1} and beta_out = M_{r+1} ...
+//     M_{G-1} 1 (the down-sweep of §8(a) a4: vector x matrix products with the lagged
+//     normaliser of tiny_sweep, on the two recursion warps) and
+//  5. runs fb_tiny's local forward / backward recursions from them over its own L_r edges
+//     with the marginals pipelined on the other warps (tiny.cuh), so the serial depth is
+//     2 L_r + (G - 2) vector x matrix steps instead of Eb.
+//
+// Measured (B200, cfg2 B=32 N=25 C=20, G=4, phase clocks in tools/phase_cscan.cu): prepass
+// ~2000 cycles, summary ~3900 (6 row-chain steps at ~650 cycles: each SM runs 21 chains over
+// the same tiles; a balanced tree of 3xTF32 mma.sync products measured ~5400, a SIMT tree
+// ~6100 — per-level latency, and instruction-fetch stalls dominated), exchange ~450, boundary
+// chains <= 3 steps, local sweeps ~1500, tail ~300: 6.8 us/step in the bench's CUDA graph vs
+// 6.25 us/step for the one-CTA fb_tiny, which therefore stays the default plan.
+//
+// Exactness.  The products are plain fp32 sums of non-negative terms, so every entry is
+// accurate to a few ulp unless flush-to-zero dropped terms; an entry >= 2^-100 (the gate)
+// bounds the dropped part by C 2^-126 / 2^-100 < 2^-21 relative, and then every vector
+// built from the summaries inherits the same bound.  Any summary entry below the gate, a
+// NaN / +inf potential, or a sequence too short to chunk (Eb < 2G), or BADLEN, sends the
+// whole sequence to CTA 0, which runs fb_tiny's exact body (tiny_body: gated steps redone
+// in log space with the per-cell max of §6(c)) while the other CTAs leave.  The decision
+// needs no extra round trip: the gate bits travel in the summary headers, so every CTA
+// sees the same set.  logZ comes from CTA G-1's forward sweep plus the fp64 offset
+// carried along the alpha chain; the marginals use the per-edge normaliser Z_t of tiny.cuh.
+#include "tiny.cuh"
+
+namespace tsb {
+
+#ifdef TS_PHASE_TIMING
+__device__ long long g_cs_phase[64][16];
+#define CSPH(k)                                                                   \
+  do {                                                                            \
+    if (threadIdx.x == 0 && blockIdx.x < 64) g_cs_phase[blockIdx.x][k] = clock64(); \
+  } while (0)
+#define CSPHW(k)                                                                         \
+  do {                                                                                   \
+    if ((threadIdx.x & 31) == 0 && blockIdx.x < 64) g_cs_phase[blockIdx.x][k] = clock64(); \
+  } while (0)
+#else
+#define CSPH(k) \
+  do {          \
+  } while (0)
+#define CSPHW(k) \
+  do {           \
+  } while (0)
+#endif
+
+namespace {
+
+constexpr float kSumGate = 7.888609052210118e-31f;  // 2^-100
+
+// Relaxed arrive: the only cross-CTA data (summaries) travel by bulk copy and are observed
+// through the receiver's mbarrier, and the mbarrier initialisation is published by
+// fence.mbarrier_init.release.cluster; the barrier only has to order "initialised" before
+// "copy into it" and "received" before "exit".  (A .release arrive costs ~1000 cycles.)
+__device__ __forceinline__ void cluster_arrive() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// one bulk copy of `bytes` from this CTA's shared memory into CTA `rank`'s copy of `dst`,
+// completing (complete_tx) on that CTA's copy of `bar`
+__device__ __forceinline__ void bulk_to_peer(float* dst, const float* src, uint32_t bytes,
+                                             uint64_t* bar, int rank) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          mapa_u32(dst, rank)),
+      "r"(smem_u32(src)), "r"(bytes), "r"(mapa_u32(bar, rank))
+      : "memory");
+}
+
+// A matrix in the cluster layout is a pair of blocks of MB = TB + 4 floats: the transposed
+// layout (row j = column j, spare row C = row sums) at offset h, the row-major layout (spare
+// row C = column sums) at h + MB; floats [TB, TB+4) of a block are the message header
+// (fp64 natural offset, uint32 flags).
+__host__ __device__ constexpr int cs_mb(int C) { return (C + 1) * tiny_rs(C) + 4; }
+
+struct CsLayout {
+  int64_t raw, ex, T, msg, rx, F, HF, G, HG, cf, vb, bar, total, tiny;  // float offsets
+  int lm;
+};
+
+// lm = max chunk length ceil(E / G); the fallback region `tiny` holds tiny_layout(N, C).
+__host__ __device__ inline CsLayout cs_layout(int64_t N, int C, int G) {
+  CsLayout l;
+  const int64_t E = N - 1 > 0 ? N - 1 : 1;
+  const int lm = (int)((E + G - 1) / G);
+  const int64_t MB = cs_mb(C), CC = (int64_t)C * C;
+  auto a4 = [](int64_t v) { return (v + 3) & ~(int64_t)3; };
+  l.lm = lm;
+  l.raw = 0;                           // [lm][C][C] bulk-copy target
+  l.ex = l.raw + lm * CC;              // [lm] x (EXF block, EXB block)
+  l.T = l.ex + lm * 2 * MB;            // [lm]
+  l.msg = a4(l.T + lm);                // the chunk summary (both blocks, with headers)
+  l.rx = l.msg + 2 * MB;               // [G] received summaries (one block each)
+  l.F = l.rx + G * MB;                 // [lm+1][32] node vectors (tiny_sweep)
+  l.HF = l.F + (lm + 1) * 32;
+  l.G = l.HF + (lm + 1) * 32;
+  l.HG = l.G + (lm + 1) * 32;
+  l.cf = l.HG + (lm + 1) * 32;         // [lm]
+  l.vb = a4(l.cf + lm);                // row-chain / boundary broadcast buffers (<= 384 floats)
+  l.bar = l.vb + 12 * 32 * 3;                   // mbarriers ld[lm], fn[lm+1], bn[lm+1], xbar + flags
+  l.total = l.bar + 2 * (lm + 2 * (lm + 1) + 1) + 8;
+  l.tiny = (l.total + 31) & ~(int64_t)31;
+  l.total = l.tiny + tiny_layout(N, C).total;
+  return l;
+}
+
+// Chunk summary by row chains: row i < C of M = EX_0 ... EX_{L-1} is the forward vector
+// e_i^T M, row C (the column sums) is 1^T M; warp w runs the rows w, w + W, ... (W warps) as
+// R = ceil((C+1)/W) interleaved vector x matrix chains of L steps, lane j <= C holding entry
+// j (lane C: the row sum, through EXF's spare row).  No normalisation inside a chunk (entries
+// stay in [2^-100, C^(L-1)] or the gate trips), so the chains are independent and need no
+// block barrier.  Writes M's row-major block mb (row C = column sums) and transposed block mf
+// (row C = row sums).  Returns true if any matrix entry of any step fell below 2^-100 (or
+// was NaN).
+template <int C, int TS, int W>
+__device__ __forceinline__ bool cs_summary_rows(const float* __restrict__ EXF, float* __restrict__ mf,
+                                                float* __restrict__ mb, float* __restrict__ vb, int L,
+                                                int warp, int lane) {
+  constexpr int RS = tiny_rs(C), Q = C / 4, R = (C + 1 + W - 1) / W;
+  const bool act = lane < C, live = lane <= C;
+  const int row = live ? lane : 0;
+  if (warp > C || warp >= W) return false;
+  float u[R];
+#pragma unroll
+  for (int m = 0; m < R; ++m) {  // start: e_r (lane C: 1) or, for row C, the ones vector
+    const int r = warp + W * m;
+    u[m] = (r == C) ? (act ? 1.f : (lane == C ? (float)C : 0.f)) : (lane == r || lane == C ? 1.f : 0.f);
+    if (!live || r > C) u[m] = 0.f;
+  }
+  bool gate = false;
+  const float* mp = EXF + row * RS;
+  for (int k = 0; k < L; ++k, mp += TS) {
+#pragma unroll
+    for (int m = 0; m < R; ++m) vb[32 * m + lane] = u[m];
+    __syncwarp();
+    float sa[R][4];
+#pragma unroll
+    for (int m = 0; m < R; ++m) sa[m][0] = sa[m][1] = sa[m][2] = sa[m][3] = 0.f;
+#pragma unroll
+    for (int c = 0; c < Q; ++c) {
+      const float4 w = *reinterpret_cast<const float4*>(mp + 4 * c);
+#pragma unroll
+      for (int m = 0; m < R; ++m) {
+        const float4 x = *reinterpret_cast<const float4*>(vb + 32 * m + 4 * c);
+        sa[m][0] = fmaf(x.x, w.x, sa[m][0]);
+        sa[m][1] = fmaf(x.y, w.y, sa[m][1]);
+        sa[m][2] = fmaf(x.z, w.z, sa[m][2]);
+        sa[m][3] = fmaf(x.w, w.w, sa[m][3]);
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int m = 0; m < R; ++m) {
+      const bool rv = warp + W * m <= C;
+      u[m] = (live && rv) ? (sa[m][0] + sa[m][1]) + (sa[m][2] + sa[m][3]) : 0.f;
+      gate |= act && rv && !(u[m] >= kSumGate);
+    }
+  }
+  // row r -> row-major block; transposed block gets column r (lanes < C) and, for r < C,
+  // the row sum (lane C) in its spare row; row C of the row-major block = column sums
+  if (live) {
+#pragma unroll
+    for (int m = 0; m < R; ++m) {
+      const int r = warp + W * m;
+      if (r > C) break;
+      if (lane < C) mb[r * RS + lane] = u[m];
+      if (r < C) mf[(lane < C ? lane * RS : C * RS) + r] = u[m];
+    }
+  }
+  return gate;
+}
+
+// Boundary chain (a4): the lane's entry of u_K for u_0 = 1 (log-one), u_{k+1} = (u_k M_{q_k}) / U_k
+// (FWD: q = q0, q0+1, ..., q1-1 over transposed blocks; !FWD: M u, q = q1-1, ..., q0 over
+// row-major blocks), U_k = Σ u_k computed by the spare lane C in the same instruction
+// stream.  Lane C returns Σ u_K, lanes > C return 0.  FWD also accumulates the natural
+// offset A (alpha_true = e^A u_K): A += off(M) + ln U_k per step.
+template <bool FWD, int C>
+__device__ __forceinline__ float cs_chain(const float* __restrict__ rx, int q0, int q1,
+                                          float* __restrict__ vb, int lane, double* A_out) {
+  constexpr int RS = tiny_rs(C), Q = C / 4, MB = cs_mb(C), TB = MB - 4;
+  const bool live = lane <= C;
+  const int row = live ? lane : 0;
+  float u = lane < C ? 1.f : (lane == C ? (float)C : 0.f);
+  double A = 0.0;
+  for (int k = 0; k < q1 - q0; ++k) {
+    const int q = FWD ? q0 + k : q1 - 1 - k;
+    const float* M = rx + (int64_t)q * MB;
+    vb[lane] = u;
+    __syncwarp();
+    float4 x[Q];
+#pragma unroll
+    for (int c = 0; c < Q; ++c) x[c] = *reinterpret_cast<const float4*>(vb + 4 * c);
+    const float U = vb[C];
+    const float* mr = M + row * RS;
+    float sa[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int c = 0; c < Q; ++c) {
+      const float4 w = *reinterpret_cast<const float4*>(mr + 4 * c);
+      sa[0] = fmaf(x[c].x, w.x, sa[0]);
+      sa[1] = fmaf(x[c].y, w.y, sa[1]);
+      sa[2] = fmaf(x[c].z, w.z, sa[2]);
+      sa[3] = fmaf(x[c].w, w.w, sa[3]);
+    }
+    const float un = ((sa[0] + sa[1]) + (sa[2] + sa[3])) * __fdividef(1.f, U);
+    if (FWD) A += *reinterpret_cast<const double*>(M + TB) + kLn2 * (double)lg2(U);
+    __syncwarp();
+    u = live ? un : 0.f;
+  }
+  *A_out = A;
+  return u;
+}
+
+}  // namespace
+
+#ifndef CS_SUM_WARPS
+#define CS_SUM_WARPS 6
+#endif
+constexpr int kSumWarps = CS_SUM_WARPS;  // warps running the summary row chains
+constexpr int kSumRows = (28 + 1 + kSumWarps - 1) / kSumWarps;  // max rows per warp (C <= 28)
+
+template <int C, int G>
+__global__ void __launch_bounds__(kTinyThreads, 1) fb_cscan_kernel(SmallArgs a) {
+  extern __shared__ __align__(16) float sm[];
+  constexpr int CC = C * C, Q4 = CC / 4, MB = cs_mb(C), TB = MB - 4, TS = 2 * MB;
+  const int64_t N = a.N, E = N - 1;
+  const int r = (int)cluster_rank();
+  const int64_t b = blockIdx.x / G;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const CsLayout Lay = cs_layout(N, C, G);
+  const int lm = Lay.lm;
+  float* raw = sm + Lay.raw;
+  float* EXF = sm + Lay.ex;  // tile t: EXF block at EXF + t TS, EXB block at + MB
+  float* EXB = EXF + MB;
+  float* Tm = sm + Lay.T;
+  float* msg = sm + Lay.msg;  // [transposed block][row-major block]
+  float* rx = sm + Lay.rx;
+  float* F = sm + Lay.F;
+  float* HF = sm + Lay.HF;
+  float* Gv = sm + Lay.G;
+  float* HG = sm + Lay.HG;
+  float* cf = sm + Lay.cf;
+  float* vb = sm + Lay.vb;
+  uint64_t* ld = reinterpret_cast<uint64_t*>(sm + Lay.bar);
+  uint64_t* fn = ld + lm;
+  uint64_t* bn = fn + lm + 1;
+  uint64_t* xbar = bn + lm + 1;
+  unsigned* sflag = reinterpret_cast<unsigned*>(xbar + 1);
+
+  // ---- prologue: barriers, the receive mbarrier armed for G-1 summaries, cluster arrive ----
+  for (int k = tid; k < 3 * lm + 3; k += kTinyThreads)
+    mbar_init(k < lm ? &ld[k] : (k < 2 * lm + 1 ? &fn[k - lm] : (k < 3 * lm + 2 ? &bn[k - 2 * lm - 1] : xbar)),
+              1);
+  if (tid == 0) sflag[0] = 0u;
+  fence_mbar_init();
+  __syncthreads();
+  if (tid == 0) mbar_expect_tx(xbar, (uint32_t)((G - 1) * MB * 4));
+  cluster_arrive();  // phase 1: my barriers exist (peers copy into them after phase 1)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (lane == 0 && a.pot) {  // L2 prefetch of this CTA's share (by the full length; a hint)
+    const int64_t p0 = (int64_t)r * E / G, p1 = (int64_t)(r + 1) * E / G;
+    for (int64_t t = p0 + warp; t < p1; t += kTinyWarps)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.pot + (b * E + t) * CC),
+                   "r"((uint32_t)(CC * 4))
+                   : "memory");
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  CSPH(0);
+
+  const int64_t len = seq_len(a.lengths, b, N);
+  const int Eb = (int)(len - 1);
+  if (len < 0 || Eb < 2 * G) {  // BADLEN or too short to chunk: CTA 0 runs the whole sequence
+    cluster_wait();
+    if (r == 0) tiny_body<C, false>(a, b, sm + Lay.tiny);
+    return;
+  }
+  const int s = (int)((int64_t)r * Eb / G), L = (int)((int64_t)(r + 1) * Eb / G) - s;
+  const float* src = a.pot + (b * E + s) * CC;
+  if (lane == 0 && warp < L)
+    bulk_load(raw + (int64_t)warp * CC, src + (int64_t)warp * CC, (uint32_t)(CC * 4), &ld[warp]);
+
+  // ---- 1. prepass (tile t on warp t) ------------------------------------------------------
+  tiny_prepass<C, TS>(raw, EXF, EXB, Tm, ld, sflag, L, warp, kTinyWarps, lane);
+  __syncthreads();
+  CSPH(1);
+  unsigned bad = sflag[0] & (unsigned)TS_F_NONFINITE;
+
+  // ---- 2. chunk summary: row chains (one loop per warp, no block barrier inside) -----------
+  if (__syncthreads_or(cs_summary_rows<C, TS, kSumWarps>(EXF, msg, msg + MB, vb + 32 * kSumRows * warp, L, warp, lane)))
+    bad |= 0x100u;
+  if (tid == 0) {
+    double off = 0.0;
+    for (int t = 0; t < L; ++t) off += (double)Tm[t];
+    *reinterpret_cast<double*>(msg + TB) = off;
+    *reinterpret_cast<double*>(msg + MB + TB) = off;
+    reinterpret_cast<unsigned*>(msg + TB)[2] = bad;
+    reinterpret_cast<unsigned*>(msg + MB + TB)[2] = bad;
+  }
+  CSPH(2);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> bulk copy
+  cluster_wait();
+  CSPH(3);  // phase 1 complete: every peer's receive barrier is armed; also a CTA barrier
+
+  // ---- 3. exchange: one bulk copy per peer ----------------------------------------------------
+  if (tid == 0) {
+#pragma unroll
+    for (int q = 0; q < G; ++q)
+      if (q != r) bulk_to_peer(rx + (int64_t)r * MB, q > r ? msg : msg + MB, (uint32_t)(MB * 4), xbar, q);
+  }
+  mbar_wait(xbar, 0);
+  CSPH(4);
+  cluster_arrive();  // phase 2: everything addressed to this CTA has landed
+#pragma unroll
+  for (int q = 0; q < G; ++q)
+    if (q != r) bad |= reinterpret_cast<const unsigned*>(rx + (int64_t)q * MB + TB)[2];
+  if (bad) {  // a gate, NaN or +inf anywhere in the sequence: CTA 0 recomputes it exactly
+    if (r == 0) tiny_body<C, false>(a, b, sm + Lay.tiny);
+    cluster_wait();
+    return;
+  }
+
+  // ---- 4./5. boundary vectors, local sweeps, marginals ------------------------------------
+  float* mg = a.marg ? a.marg + (b * E + s) * CC : nullptr;
+  if (warp == kFwdWarp) {
+    double Ain;
+    const float v0 = cs_chain<true, C>(rx, 0, r, vb, lane, &Ain);
+    CSPHW(5);
+    const int kbf = tiny_sweep<true, C, TS>(EXF, raw, Tm, F, HF, cf, fn, L, lane, v0);
+    CSPHW(6);
+    if (r == G - 1) {  // logZ = A_in + Σ_t (T_t + ln2 c_t) + ln2 log2 Σ_j u_L[j]
+      double part = 0.0;
+      for (int t = lane; t < L; t += 32)
+        part += (double)Tm[t] + kLn2 * (double)(t < kbf ? lg2(F[t * 32 + C]) : cf[t]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+      const float Lf = warp_lse2(lane < C ? node_log(F, HF, L, lane) : neg_inf());
+      if (lane == 0) {
+        const bool empty = (Lf == neg_inf()) || !(part > -INFINITY);
+        a.logz[b] = empty ? neg_inf() : (float)(Ain + part + kLn2 * (double)Lf);
+        if (a.flags) a.flags[b] = empty ? (unsigned)TS_F_EMPTY : 0u;
+      }
+    }
+  } else if (warp == kBwdWarp) {
+    if (mg) {
+      double unused;
+      const float v0 = cs_chain<false, C>(rx, r + 1, G, vb + 32, lane, &unused);
+      CSPHW(7);
+      tiny_sweep<false, C, TS>(EXB, raw, Tm, Gv, HG, nullptr, bn, L, lane, v0);
+      CSPHW(8);
+    }
+  } else if (mg) {
+#ifdef CS_NO_WORKERS
+    if (true) {} else
+#endif
+    {
+    const int wi = worker_index(warp);
+    tiny_marginals<C, TS>(EXB, raw, Tm, F, HF, Gv, HG, fn, bn, L, mg, wi, kWorkers, lane);
+    if (r == G - 1) {  // edges beyond the sequence: mu = 0
+      float4* m0 = reinterpret_cast<float4*>(a.marg + b * E * CC);
+      for (int64_t k = (int64_t)Eb * Q4 + (32 * wi + lane); k < E * Q4; k += 32 * kWorkers)
+        m0[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    }
+  }
+#ifdef TS_PHASE_TIMING
+  __syncthreads();
+  CSPH(9);
+#endif
+  cluster_wait();  // phase 2: peers no longer copy out of this CTA's shared memory
+}
+
+// ====================================================================================
+// host side
+// ====================================================================================
+size_t cscan_smem_bytes(int64_t N, int64_t C, int G) {
+  return (size_t)cs_layout(N, (int)C, G).total * sizeof(float);
+}
+
+constexpr size_t kCscanSmemMax = 227 * 1024;
+
+bool cscan_fits(const SmallArgs& a, int G) {
+  if (G != 2 && G != 4) return false;
+  if (!tiny_fits(a)) return false;  // C % 4 == 0, C <= 28, alignment, the fallback's smem
+  const int64_t E = a.N - 1;
+  if (E < 2 * G || E > 8 * G) return false;  // chunks of 2..8 edges (tree depth <= 3)
+  return cscan_smem_bytes(a.N, a.C, G) <= kCscanSmemMax;
+}
+
+int cscan_g(const SmallArgs& a, int sms) {
+  for (int G : {4, 2})
+    if (a.B * G <= sms && cscan_fits(a, G)) return G;
+  return 0;
+}
+
+namespace {
+template <int C, int G>
+cudaError_t launch_cs(const SmallArgs& a, size_t smem, cudaStream_t st) {
+  static std::atomic<uint64_t> mask{0};
+  cudaError_t e = smem_optin_once(fb_cscan_kernel<C, G>, mask, (int)kCscanSmemMax);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(a.B * G));
+  cfg.blockDim = dim3(kTinyThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = G;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelEx(&cfg, fb_cscan_kernel<C, G>, a);
+}
+template <int G>
+cudaError_t launch_cs_g(const SmallArgs& a, size_t smem, cudaStream_t st) {
+  switch (a.C) {
+    case 4: return launch_cs<4, G>(a, smem, st);
+    case 8: return launch_cs<8, G>(a, smem, st);
+    case 12: return launch_cs<12, G>(a, smem, st);
+    case 16: return launch_cs<16, G>(a, smem, st);
+    case 20: return launch_cs<20, G>(a, smem, st);
+    case 24: return launch_cs<24, G>(a, smem, st);
+    case 28: return launch_cs<28, G>(a, smem, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+}  // namespace
+
+cudaError_t launch_cscan(const SmallArgs& a, int G, cudaStream_t st) {
+  const size_t smem = cscan_smem_bytes(a.N, a.C, G);
+  if (G == 4) return launch_cs_g<4>(a, smem, st);
+  if (G == 2) return launch_cs_g<2>(a, smem, st);
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace tsb

@@ -28,10 +28,11 @@ cudaError_t launch_small(const SmallArgs& a, cudaStream_t st);
 size_t tiny_smem_bytes(int64_t N, int64_t C);
 bool tiny_fits(const SmallArgs& a);
 cudaError_t launch_tiny(const SmallArgs& a, cudaStream_t st);
-int cluster_g(int64_t B, int64_t N, int sms);
-size_t cluster_smem_bytes(int64_t N, int64_t C, int G);
-bool cluster_fits(int64_t N, int64_t C, int G);
-cudaError_t launch_cluster(const SmallArgs& a, int G, cudaStream_t st);
+// the chunked scan of §6(a) on a G-CTA cluster per sequence (fb_cscan.cu), same shapes
+size_t cscan_smem_bytes(int64_t N, int64_t C, int G);
+bool cscan_fits(const SmallArgs& a, int G);
+int cscan_g(const SmallArgs& a, int sms);  // G for the auto plan (0 = do not use)
+cudaError_t launch_cscan(const SmallArgs& a, int G, cudaStream_t st);
 
 // ---- streaming (time-chunked) forward / backward sweeps, log semiring (C <= 128) ----
 // Chunk k of sequence b covers edges [k*L, min((k+1)*L, E_b)), E_b = len_b - 1.

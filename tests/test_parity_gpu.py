@@ -409,7 +409,8 @@ def test_host_pipeline_binding_changes(dev):
 
 @pytest.mark.parametrize("G", [2, 4])
 def test_cluster_dsmem_variant(dev, G):
-    """The chunked-scan variant for short chains on a G-CTA cluster (DSMEM summary exchange)."""
+    """The chunked-scan plan for short chains on a G-CTA cluster (fb_cscan.cu: chunk
+    summaries exchanged by DSMEM bulk copies); shapes it cannot chunk run one CTA."""
     try:
         tsb.set_small_cluster(G)
         for (B, N, C) in [(32, 25, 20), (3, 40, 7), (2, 17, 32)]:

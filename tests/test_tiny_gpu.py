@@ -1,7 +1,9 @@
-"""GPU parity of the latency-optimised short-chain kernel (fb_tiny.cu: C % 4 == 0, C <= 28)
-against the fp64 oracle, and against the general single-CTA kernel (fb_small.cu) it
-replaces on those shapes.  Gates as everywhere: logZ 1e-5 relative,
-marginals 1e-4 absolute, flags identical.
+"""GPU parity of the latency-optimised short-chain kernels (C % 4 == 0, C <= 28) against the
+fp64 oracle, and against the general single-CTA kernel (fb_small.cu) they replace on those
+shapes: every test runs three times — one CTA per sequence (fb_tiny.cu) and the §6(a)
+chunked scan on a 2- and a 4-CTA cluster per sequence (fb_cscan.cu; shapes it cannot chunk,
+and gated / non-finite sequences, take its in-launch exact fallback).  Gates as everywhere
+(DESIGN.md §5): logZ 1e-5 relative, marginals 1e-4 absolute, flags identical.
 """
 import numpy as np
 import pytest
@@ -15,6 +17,13 @@ from _util import check_logz, check_marg
 pytestmark = pytest.mark.gpu
 
 TINY_C = [4, 8, 12, 16, 20, 24, 28]
+
+
+@pytest.fixture(autouse=True, params=[0, 2, 4], ids=["tiny", "cscan2", "cscan4"])
+def plan(request):
+    tsb.set_small_cluster(request.param)
+    yield request.param
+    tsb.set_small_cluster(0)
 
 
 @pytest.fixture
@@ -108,3 +117,30 @@ def test_tiny_cfg2_sum_to_one_and_deterministic(dev):
     assert float((s - 1).abs().max()) < 1e-5
     m2, lz2, fl2 = tsb.marginals(pot)
     assert torch.equal(m, m2) and torch.equal(lz, lz2)
+
+
+def test_plan_knob_selects_kernel_for_cfg2(dev, plan):
+    """cfg2 (B=32, N=25, C=20): the auto plan (-1) runs the chunked scan on 4-CTA clusters,
+    the default (0) one CTA per sequence."""
+    pot = torch.from_numpy(tsgen.config_potentials(tsgen.CONFIGS[2])).to(dev)
+    tsb.set_small_cluster(-1)
+    tsb.marginals(pot)
+    assert tsb.last_kernel() == "fb_cscan_kernel"
+    tsb.set_small_cluster(0)
+    tsb.marginals(pot)
+    assert tsb.last_kernel() == "fb_tiny_kernel"
+
+
+@pytest.mark.parametrize("C", [12, 20])
+def test_mixed_fast_and_fallback_sequences(dev, C):
+    """One batch where some clusters take the fast chunked path and others fall back
+    in-launch (a gated hidden path, a NaN, a sequence too short to chunk)."""
+    B, N = 8, 33
+    pot = tsgen.potentials(B, N, C, seed=90 + C, s=10)
+    lengths = np.full(B, N, dtype=np.int32)
+    pot[1, 9, :, 2] = -200.0
+    pot[1, 10, 2, :] = 200.0 + pot[1, 10, 2, :]
+    pot[3, 20, 0, 1] = np.nan
+    lengths[5] = 4
+    lengths[6] = 2 * 4 + 1
+    parity(pot.astype(np.float32), lengths, dev)
