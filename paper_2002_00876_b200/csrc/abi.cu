@@ -93,6 +93,32 @@ int device_sms() {
   return sms;
 }
 
+// Chunk length of the auto plan, 0 = serial (P = 1).  Calibrated on B200 (tools/plan_calib.py,
+// profiles/r2_plan_calib.jsonl; ms = one ts_marginals call):
+//   serial:  meet64 (C = 64) ~1.2 us per edge, fwd2+bwd2 ~2.6 us (C <= 32) / ~4.9 us (C = 128)
+//            per edge, times ceil(B / #SMs) waves;
+//   chunked: C <= 64 (SIMT summaries, C^3 per edge): ~0.39 + 4.5e-5 B E ms (C = 64) and
+//            ~0.45 + 1.1e-5 B E ms (C = 32) with L = 64 (the best of 32..1024 in every shape);
+//            C = 128 (tensor-core summaries): best L = E / floor(#SMs / B), at least 128
+//            (one wave of chunk summaries; cfg5: 37 chunks of 1772 edges, 17.7 ms, vs 32
+//            chunks of 2048, 20.1 ms).
+// The serial plan wins for C = 64 once B >~ 30 (e.g. every per-rank shape of cfg3's batch
+// sharding: B = 256 / G); chunking pays for few long sequences (cfg5).
+int64_t auto_chunk(int64_t B, int64_t E, int64_t C, int sms) {
+  if (E < 64) return 0;
+  const double waves = (double)((B + sms - 1) / sms);
+  if (C > 64) {
+    if (2 * B > sms) return 0;
+    const int64_t per = sms / B;  // chunks per sequence that keep one wave of summaries
+    const int64_t L = (E + per - 1) / per;
+    return L < 128 ? 128 : L;
+  }
+  const bool meet = (C == 64);
+  const double serial_ms = (meet ? 1.2e-3 : 2.6e-3) * (double)E * waves;
+  const double chunk_ms = (C > 32 ? 0.39 + 4.5e-5 * (double)(B * E) : 0.45 + 1.1e-5 * (double)(B * E));
+  return chunk_ms < serial_ms ? 64 : 0;
+}
+
 Plan log_plan(const ts_chain* c) {
   const int64_t knob = g_plan_chunk.load();
   const int64_t E = c->N - 1;
@@ -104,11 +130,8 @@ Plan log_plan(const ts_chain* c) {
       return p;
     }
     const int sms = device_sms();
-    if (c->B < sms && E >= 64) {
-      P = (sms + c->B - 1) / c->B;
-      const int64_t cap = (E + 31) / 32;  // chunks of at least 32 edges
-      if (P > cap) P = cap;
-    }
+    const int64_t L = auto_chunk(c->B, E, c->C, sms);
+    if (L > 0 && L < E) P = (E + L - 1) / L;
   } else if (knob < E) {
     P = (E + knob - 1) / knob;
   } else if (small_fits(c->N, c->C)) {

@@ -346,7 +346,7 @@ bool vit2_ok(const VitArgs& a) {
          a.N > 1 && a.B * (a.N - 1) * a.C < ((int64_t)1 << 31);
 }
 
-// cluster size: the largest G in {1, 2, 4, 8} with B*G <= #SMs (C/G >= 32 columns per CTA),
+// cluster size: the largest G in {1, 2, 4} with B*G <= #SMs (C/G >= 32 columns per CTA),
 // or the debug override g_force (0 = auto).
 cudaError_t launch_vit2(const VitArgs& a, int g_force, cudaStream_t st) {
   int sms = 148, dev = 0;
@@ -355,7 +355,9 @@ cudaError_t launch_vit2(const VitArgs& a, int g_force, cudaStream_t st) {
   if (g_force > 0) {
     G = g_force;
   } else {
-    const int gmax = (int)(a.C / 32) < 8 ? (int)(a.C / 32) : 8;
+    // at most 4 CTAs per sequence: G = 8 measured slower than G = 4 at every batch
+    // (cfg4 shape, B = 8..64; profiles/r2_shard_shapes.jsonl)
+    const int gmax = (int)(a.C / 32) < 4 ? (int)(a.C / 32) : 4;
     while (2 * G <= gmax && a.B * 2 * G <= sms) G *= 2;
   }
   if (a.C == 256) {

@@ -128,3 +128,16 @@ def test_tensor_core_summaries_gate(dev, mode):
         check_plan(20.0 * tsgen.potentials(2, 60, 128, seed=4), None, dev, [8])
     finally:
         tsb.set_tc_summary(3)
+
+
+@pytest.mark.parametrize("G", [1, 2, 4, 8])
+def test_auto_plan_per_rank_cfg3_keeps_meet64(dev, G):
+    """Batch sharding of cfg3 over G ranks (B = 256 / G per rank, N = 512, C = 64): the auto
+    plan keeps the one-read-per-sweep meet-in-the-middle kernel on every per-rank batch (the
+    chunked SIMT scan measured 4.7x slower at B = 128; abi.cu auto_chunk)."""
+    cfg = tsgen.CONFIGS[3]
+    tsb.set_plan_chunk(0)
+    pot = torch.empty((cfg.B // G, cfg.E, cfg.C, cfg.C), dtype=torch.float32, device=dev)
+    tsgen.fill_torch(pot, cfg)
+    tsb.marginals(pot)
+    assert tsb.last_kernel() == "meet64_kernel"
