@@ -111,6 +111,31 @@ def time_sharded_viterbi(local_pot, edge_begin: int, n_global: int, group=None, 
     return path, score, flags
 
 
-def batch_sharded(fn, pot_local, *args, **kw):
-    """Batch sharding needs no collective: each rank runs `fn` on its own slice."""
-    return fn(pot_local, *args, **kw)
+def all_gather_batch(t: torch.Tensor, B_global: int, group=None) -> torch.Tensor:
+    """Concatenate every rank's batch slice (rank r holds rows shard_batch(B_global, world, r))
+    into the global [B_global, ...] tensor on every rank: slices are padded to the largest
+    shard, all-gathered once, and cut back in rank order."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    b0, b1 = shard_batch(B_global, world, rank)
+    assert t.shape[0] == b1 - b0, (t.shape, b0, b1)
+    cmax = max(shard_range(B_global, world, r)[1] for r in range(world))
+    pad = torch.zeros((cmax,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+    pad[: t.shape[0]] = t
+    g = _all_gather(pad, group)  # [world, cmax, ...]
+    return torch.cat([g[r, : shard_range(B_global, world, r)[1]] for r in range(world)])
+
+
+def batch_sharded(fn, pot_local, *args, B_global: int | None = None, group=None, **kw):
+    """Batch sharding: sequences are independent, so each rank runs `fn` on its
+    own contiguous slice (shard_batch) with no collective on the data path.  With
+    `B_global` set, every tensor `fn` returns (leading dimension = the local batch) is
+    all-gathered into the global batch afterwards (all_gather_batch) — an output gather,
+    not part of the computation."""
+    out = fn(pot_local, *args, **kw)
+    if B_global is None:
+        return out
+    if isinstance(out, torch.Tensor):
+        return all_gather_batch(out, B_global, group)
+    return tuple(all_gather_batch(o, B_global, group) if isinstance(o, torch.Tensor) else o
+                 for o in out)

@@ -194,3 +194,36 @@ def test_time_sharded_viterbi_gloo_world2(tmp_path, B, N, C):
              join=True)
     for r in range(world):
         assert open(tmp_path / f"v{r}").read() == "1 1", r
+
+
+def _bworker(rank, world, port, B, N, C, seed, result_dir):
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    try:
+        pot = tsgen.potentials(B, N, C, seed)
+        b0, b1 = tdist.shard_batch(B, world, rank)
+
+        def fn(p):  # per-rank compute (fp64 oracle: test infrastructure)
+            lz, mg, fl = oracle.chain_marginals(p.numpy())
+            return torch.from_numpy(mg), torch.from_numpy(lz), torch.from_numpy(fl.astype(np.int32))
+
+        mg, lz, fl = tdist.batch_sharded(fn, torch.from_numpy(np.ascontiguousarray(pot[b0:b1])),
+                                         B_global=B)
+        lz_ref, mg_ref, fl_ref = oracle.chain_marginals(pot)
+        ok = (np.array_equal(lz.numpy(), lz_ref) and np.array_equal(mg.numpy(), mg_ref)
+              and np.array_equal(fl.numpy(), fl_ref.astype(np.int32)))
+        with open(os.path.join(result_dir, f"b{rank}"), "w") as f:
+            f.write(f"{int(ok)}")
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("B", [5, 2])
+def test_batch_sharded_gather_gloo_world2(tmp_path, B):
+    """Uneven batch shards (B = 5 over 2 ranks; B = 2) gathered back into the global batch,
+    bit-identical to the unsharded computation."""
+    world = 2
+    mp.spawn(_bworker, args=(world, _free_port(), B, 9, 3, 21, str(tmp_path)), nprocs=world,
+             join=True)
+    for r in range(world):
+        assert open(tmp_path / f"b{r}").read() == "1", r
