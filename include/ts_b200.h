@@ -192,8 +192,12 @@ TS_API ts_status ts_segment_viterbi_finish(const ts_chain *local, int64_t edge_b
  * log p(z) = Score(z) - A and linearity of expectation over the parts
  * (P:181-183):   H_b = A_b - Σ_{t,i,j} mu[b][t][i][j] l[b][t][i][j].
  * Runs the ts_marginals(TS_LOG) hot path into `marg` (required, as ts_marginals) and `logz`
- * (required), then a deterministic two-stage fp64 reduction of mu·l (terms with mu = 0
- * skipped).  entropy [B] fp32 out; NaN for EMPTY / NONFINITE / BADLEN sequences.
+ * (required) and reduces mu·l (terms with mu = 0 skipped) deterministically: fused into the
+ * marginal kernel's epilogue where the plan's kernel supports it (the one-CTA short-chain
+ * kernel: no extra launch; meet-in-the-middle C = 64: per-engine fp64 partials + a B-thread
+ * final kernel), else a two-stage fp64 reduction pass over mu and l.  Fixed thread -> element
+ * mapping and fixed reduction orders in every variant (bit-reproducible).  entropy [B] fp32
+ * out; NaN for EMPTY / NONFINITE / BADLEN sequences.
  * ws: ts_workspace_bytes(c, TS_OP_ENTROPY, TS_LOG) bytes, 256-byte aligned. */
 TS_API ts_status ts_entropy(const ts_chain *c, float *marg, float *logz, float *entropy,
                             uint32_t *flags, void *ws, size_t ws_bytes, void *stream);
@@ -203,8 +207,8 @@ TS_API ts_status ts_entropy(const ts_chain *c, float *marg, float *logz, float *
  *     out[b] = E_{z ~ p}[Σ_{t<len-1} r[b][t][z_t][z_{t+1}]] = Σ_{t,i,j} mu[b][t][i][j] r[b][t][i][j]
  * r [B][N-1][C][C] fp32 device, 16-byte aligned (same layout as pot; required, TS_E_INVALID
  * when NULL).  Runs the ts_marginals(TS_LOG) hot path into `marg` and `logz` (both required
- * as for ts_entropy), then the same deterministic two-stage fp64 reduction of mu·r (terms
- * with mu = 0 skipped, so r may hold anything at masked parts).  out [B] fp32; NaN for
+ * as for ts_entropy) and the same deterministic reduction of mu·r (fused or a separate pass,
+ * as for ts_entropy; terms with mu = 0 skipped, so r may hold anything at masked parts).  out [B] fp32; NaN for
  * EMPTY / NONFINITE / BADLEN sequences.  r = l gives E_p[Score] = A - H.
  * ws: ts_workspace_bytes(c, TS_OP_EXPECTATION, TS_LOG) bytes, 256-byte aligned. */
 TS_API ts_status ts_expectation(const ts_chain *c, const float *r, float *marg, float *logz,

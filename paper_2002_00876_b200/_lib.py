@@ -9,7 +9,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libts_b200.so")
+# TS_B200_LIB: an alternative in-tree build of the same library (kernel-variant experiments)
+LIB_PATH = os.environ.get("TS_B200_LIB") or os.path.join(_HERE, "libts_b200.so")
 
 TS_LOG, TS_MAX = 0, 1
 TS_OP_LOGZ, TS_OP_MARG, TS_OP_VITERBI, TS_OP_MARG_HOST, TS_OP_SEGMENT = 0, 1, 2, 3, 4

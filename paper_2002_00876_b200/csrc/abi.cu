@@ -280,8 +280,21 @@ ts_status cuda_status(cudaError_t e) {
   return TS_E_CUDA;
 }
 
+// A request to fuse the f1 reduction (entropy: Σ mu·l, expectation: Σ mu·r) into the marginal
+// kernel of the plan.  run_log sets `fused` when the plan's kernel did it:
+// with `final_partials` > 0 the kernel left that many fp64 partials per sequence in `partial`
+// (the caller runs the final stage), else it wrote `out` itself.
+struct FusedX {
+  int mode;          // 1 entropy, 2 expectation
+  const float* r;    // expectation feature
+  float* out;        // [B]
+  double* partial;   // [B][final_partials]
+  bool fused = false;
+  int final_partials = 0;
+};
+
 ts_status run_log(const ts_chain* c, float* marg, float* logz, uint32_t* flags, void* ws,
-                  size_t ws_bytes, cudaStream_t st) {
+                  size_t ws_bytes, cudaStream_t st, FusedX* fx = nullptr) {
   const Plan p = log_plan(c);
   if (p.kind == PlanKind::Unsupported) {
     if (c->C > 256) return TS_E_UNSUPPORTED;
@@ -309,8 +322,11 @@ ts_status run_log(const ts_chain* c, float* marg, float* logz, uint32_t* flags, 
   if (p.kind == PlanKind::Small) {
     SmallArgs a{c->pot, c->lengths, c->B, c->N, c->C, marg, logz, flags};
     const int knob = g_small_cluster.load();
+    const bool fuse = fx && marg && g_tiny.load() && tiny_fits(a);
     int G = 0;
-    if (knob < 0)
+    if (fuse)
+      G = 0;  // the fused epilogue lives in the one-CTA body
+    else if (knob < 0)
       G = g_tiny.load() ? cscan_g(a, device_sms()) : 0;
     else if (cscan_fits(a, knob))
       G = knob;
@@ -319,6 +335,13 @@ ts_status run_log(const ts_chain* c, float* marg, float* logz, uint32_t* flags, 
       r = cuda_status(launch_cscan(a, G, st));
       t_kernel = "fb_cscan_kernel";
     } else if (g_tiny.load() && tiny_fits(a)) {
+      if (fuse) {
+        a.xmode = fx->mode;
+        a.xr = fx->r;
+        a.xout = fx->out;
+        fx->fused = true;
+        fx->final_partials = 0;
+      }
       r = cuda_status(launch_tiny(a, st));
       t_kernel = "fb_tiny_kernel";
     } else {
@@ -336,6 +359,13 @@ ts_status run_log(const ts_chain* c, float* marg, float* logz, uint32_t* flags, 
   if (marg && p.P == 1 && w.beta_hat && meet_ok(c->C, c->pot, marg) && g_meet.load()) {
     MeetArgs m{c->pot, c->lengths, c->B, c->N, marg, logz, flags,
                w.alpha_hat, w.beta_hat, w.mlag, w.tmax};
+    if (fx) {
+      m.xmode = fx->mode;
+      m.xr = fx->r;
+      m.xsum = fx->partial;
+      fx->fused = true;
+      fx->final_partials = 2;  // one per engine
+    }
     if ((e = launch_meet(m, c->C, st)) != cudaSuccess) return cuda_status(e);
     t_launches = 1;
     t_kernel = "meet64_kernel";
@@ -632,7 +662,7 @@ size_t entropy_ws(const ts_chain* c, void* ws, size_t* marg_part, double** parti
   DistArgs d{};
   d.B = c->B;
   d.N = c->N;
-  const int S = entropy_slices(d);
+  const int S = entropy_slices(d) < 2 ? 2 : entropy_slices(d);  // >= 2: fused meet64 partials
   if (marg_part) *marg_part = m;
   if (partial) *partial = ws ? reinterpret_cast<double*>(static_cast<char*>(ws) + m) : nullptr;
   return m + align_up(sizeof(double) * (size_t)(c->B * S));
@@ -943,10 +973,12 @@ ts_status entropy_or_expectation(const ts_chain* c, const float* r, float* marg,
   double* partial = nullptr;
   const size_t need = entropy_ws(c, ws, &mpart, &partial);
   if (ws_bytes < need || !ws || !aligned(ws, kAlign)) return TS_E_WORKSPACE;
-  ts_status st_r = run_log(c, marg, logz, flags, ws, mpart, st);
+  FusedX fx{r ? 2 : 1, r, out, partial};
+  ts_status st_r = run_log(c, marg, logz, flags, ws, mpart, st, &fx);
   if (st_r != TS_OK) return st_r;
   const int n = t_launches;
   const char* k = t_kernel;
+  if (fx.fused && fx.final_partials == 0) return TS_OK;  // the marginal kernel wrote `out`
   DistArgs d{};
   d.pot = c->pot;
   d.lengths = c->lengths;
@@ -959,6 +991,14 @@ ts_status entropy_or_expectation(const ts_chain* c, const float* r, float* marg,
   d.out = out;
   d.r = r;
   d.partial = partial;
+  if (fx.fused) {  // per-sequence partials from the marginal kernel: the final stage only
+    st_r = cuda_status(launch_entropy_final(d, fx.final_partials, st));
+    if (st_r == TS_OK) {
+      t_launches = n + 1;
+      t_kernel = k;
+    }
+    return st_r;
+  }
   st_r = cuda_status(launch_entropy(d, st));
   if (st_r == TS_OK) {
     t_launches = n + 2;

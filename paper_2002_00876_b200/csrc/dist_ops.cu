@@ -226,6 +226,11 @@ cudaError_t launch_entropy(DistArgs a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+cudaError_t launch_entropy_final(const DistArgs& a, int S, cudaStream_t st) {
+  entropy_final_kernel<<<(unsigned)((a.B + 127) / 128), 128, 0, st>>>(a, S);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_score(const DistArgs& a, cudaStream_t st) {
   score_kernel<<<(unsigned)a.B, kRedThreads, 0, st>>>(a);
   return cudaGetLastError();

@@ -49,6 +49,7 @@ struct __align__(16) MeetSmem {
   float redlm[2][kNW];
   float redls[2][kNW];
   double O[2];
+  double xred[2][kNW];
   uint32_t bad[2];
   float Lh;
   int dead;
@@ -62,6 +63,7 @@ struct EState {
   double O;
   int64_t u;       // tiles consumed by this engine
   int64_t issued;  // tiles issued (producer thread only)
+  double xacc;     // fused f1 epilogue: this thread's Σ mu·x over its elements (fixed order)
 };
 
 __device__ __forceinline__ float4 lds4(const float* p) { return *reinterpret_cast<const float4*>(p); }
@@ -77,6 +79,17 @@ __device__ __forceinline__ void issue(MeetSmem& s, int eng, EState& st, int64_t 
   bulk_load(s.ring[eng][slot], potb + t * kCC, kTileBytes, &s.full[eng][slot]);
 }
 
+// Σ mu·x over one float4 of marginals (terms with mu = 0 skipped: masked parts may hold -inf
+// in l or anything in r, reading R13/R13b)
+__device__ __forceinline__ float xdot4(float4 mu, float4 x) {
+  float s = 0.f;
+  if (mu.x != 0.f) s = fmaf(mu.x, x.x, s);
+  if (mu.y != 0.f) s = fmaf(mu.y, x.y, s);
+  if (mu.z != 0.f) s = fmaf(mu.z, x.z, s);
+  if (mu.w != 0.f) s = fmaf(mu.w, x.w, s);
+  return s;
+}
+
 // merge the 256-thread engine's two-warp owner reductions (log2-sum-exp of kC values)
 __device__ __forceinline__ float lse_parts(const float* lm, const float* ls) {
   const float LM = fmaxf(lm[0], lm[1]);
@@ -90,7 +103,7 @@ __device__ __forceinline__ float lse_parts(const float* lm, const float* ls) {
 // ----------------------------------------------------------------------------------------
 // engine F: thread (g, q) holds rows g + 16 r (r < 4) x columns 4q..4q+3 of each tile
 // ----------------------------------------------------------------------------------------
-template <bool P2>
+template <bool P2, int XM>
 __device__ __forceinline__ void f_run(MeetSmem& s, const MeetArgs& a, EState& st, int64_t b,
                                       int64_t t_lo, int64_t t_hi, int64_t Eb, const float* potb,
                                       int e, float log2C) {
@@ -236,12 +249,17 @@ __device__ __forceinline__ void f_run(MeetSmem& s, const MeetArgs& a, EState& st
       const float L = lse_parts(s.redlm[0], s.redls[0]);
       const float c0 = ex2(bh4.x - L), c1 = ex2(bh4.y - L), c2 = ex2(bh4.z - L), c3 = ex2(bh4.w - L);
       float* mt = a.marg + ((b * E + t) * kC) * kC + 4 * q;
+      const float* xt = XM == 2 ? a.xr + ((b * E + t) * kC) * kC + 4 * q : nullptr;
+      float xe = 0.f;  // this edge's Σ mu·x over the thread's elements
       if (c0 <= kBig && c1 <= kBig && c2 <= kBig && c3 <= kBig) {
 #pragma unroll
         for (int r = 0; r < kR; ++r) {
           const float4 o = make_float4(ai[r] * c0 * v[r].x, ai[r] * c1 * v[r].y,
                                        ai[r] * c2 * v[r].z, ai[r] * c3 * v[r].w);
           __stcs(reinterpret_cast<float4*>(mt + (g + kG * r) * kC), o);
+          if (XM)
+            xe += xdot4(o, XM == 1 ? lds4(tile + (g + kG * r) * kC + 4 * q)
+                                        : __ldcs(reinterpret_cast<const float4*>(xt + (g + kG * r) * kC)));
         }
       } else {
         const float* ahv = s.ah_s[st.buf];
@@ -253,9 +271,14 @@ __device__ __forceinline__ void f_run(MeetSmem& s, const MeetArgs& a, EState& st
 #pragma unroll
           for (int k = 0; k < 4; ++k)
             o[k] = ex2(ahv[i] + (tile[i * kC + 4 * q + k] - st.Ts) * kLog2e + bhk[k] - m - L);
-          __stcs(reinterpret_cast<float4*>(mt + i * kC), make_float4(o[0], o[1], o[2], o[3]));
+          const float4 o4 = make_float4(o[0], o[1], o[2], o[3]);
+          __stcs(reinterpret_cast<float4*>(mt + i * kC), o4);
+          if (XM)
+            xe += xdot4(o4, XM == 1 ? lds4(tile + i * kC + 4 * q)
+                                         : __ldcs(reinterpret_cast<const float4*>(xt + i * kC)));
         }
       }
+      if (XM) st.xacc += (double)xe;
     }
     st.m = m_next;
     st.buf ^= 1;
@@ -267,7 +290,7 @@ __device__ __forceinline__ void f_run(MeetSmem& s, const MeetArgs& a, EState& st
 // ----------------------------------------------------------------------------------------
 // engine B: thread (q, g) holds rows 4q..4q+3 x columns 4g..4g+3 of each tile
 // ----------------------------------------------------------------------------------------
-template <bool P2>
+template <bool P2, int XM>
 __device__ __forceinline__ void b_run(MeetSmem& s, const MeetArgs& a, EState& st, int64_t b,
                                       int64_t t_lo, int64_t t_hi, int64_t Eb, const float* potb,
                                       int e, float log2C) {
@@ -314,6 +337,8 @@ __device__ __forceinline__ void b_run(MeetSmem& s, const MeetArgs& a, EState& st
     if (P2) {  // mu_t(i,j) = e_ij b_j 2^(ah_t[i] - m_t^F - L_{t+1} + m)
       const float ahr[4] = {ah4.x, ah4.y, ah4.z, ah4.w};
       float* mt = a.marg + ((b * E + t) * kC + 4 * q) * kC + 4 * g;
+      const float* xt = XM == 2 ? a.xr + ((b * E + t) * kC + 4 * q) * kC + 4 * g : nullptr;
+      float xe = 0.f;
       const float L = st.Lnext;
 #pragma unroll
       for (int rr = 0; rr < 4; ++rr) {
@@ -334,7 +359,10 @@ __device__ __forceinline__ void b_run(MeetSmem& s, const MeetArgs& a, EState& st
           o.w = ex2(cst + (v[rr].w - st.Ts) * kLog2e + bh.w);
         }
         __stcs(reinterpret_cast<float4*>(mt + rr * kC), o);
+        if (XM)
+          xe += xdot4(o, XM == 1 ? v[rr] : __ldcs(reinterpret_cast<const float4*>(xt + rr * kC)));
       }
+      if (XM) st.xacc += (double)xe;
     } else {
 #pragma unroll
       for (int rr = 0; rr < 4; ++rr) {
@@ -434,6 +462,7 @@ __device__ __forceinline__ void zero_range(float* p, int64_t n4, int tid) {
   for (int64_t x = tid; x < n4; x += kNT) __stcs(p4 + x, z);
 }
 
+template <int XM>
 __global__ void __launch_bounds__(kNT, 2) meet64_kernel(MeetArgs a) {
   extern __shared__ __align__(128) unsigned char smraw[];
   MeetSmem& s = *reinterpret_cast<MeetSmem*>(smraw);
@@ -446,6 +475,7 @@ __global__ void __launch_bounds__(kNT, 2) meet64_kernel(MeetArgs a) {
     if (tid == 0) {
       a.logz[b] = qnan();
       if (a.flags) a.flags[b] = TS_F_BADLEN;
+      if (XM) a.xsum[2 * b] = a.xsum[2 * b + 1] = 0.0;
     }
     return;
   }
@@ -472,16 +502,16 @@ __global__ void __launch_bounds__(kNT, 2) meet64_kernel(MeetArgs a) {
     }
   }
   __syncthreads();
-  EState st{qnan(), 0.f, 0.f, neg_inf(), 0, 0u, 0.0, 0, 0};
+  EState st{qnan(), 0.f, 0.f, neg_inf(), 0, 0u, 0.0, 0, 0, 0.0};
   if (e == 0)
     while (st.issued < kS && st.issued < Eb) issue(s, eng, st, Eb, potb);
   zero_range(mgb + Eb * kCC, (E - Eb) * kCC / 4, tid);
 
   // ---- phase 1 -----------------------------------------------------------------------
   if (eng == 0)
-    f_run<false>(s, a, st, b, 0, h, Eb, potb, e, log2C);
+    f_run<false, XM>(s, a, st, b, 0, h, Eb, potb, e, log2C);
   else
-    b_run<false>(s, a, st, b, h, Eb, Eb, potb, e, log2C);
+    b_run<false, XM>(s, a, st, b, h, Eb, Eb, potb, e, log2C);
   if (e == 0) s.O[eng] = st.O;
   if (st.bad) atomicOr(&s.bad[eng], 1u);
   __syncthreads();
@@ -515,6 +545,7 @@ __global__ void __launch_bounds__(kNT, 2) meet64_kernel(MeetArgs a) {
   __syncthreads();
   if (s.dead) {
     zero_range(mgb, Eb * kCC / 4, tid);
+    if (XM && tid < 2) a.xsum[2 * b + tid] = 0.0;
     if (e == 0)  // drain this engine's outstanding bulk copies before the CTA exits
       for (int64_t u = st.u; u < st.issued; ++u)
         mbar_wait(&s.full[eng][u % kS], (uint32_t)((u / kS) & 1));
@@ -522,14 +553,33 @@ __global__ void __launch_bounds__(kNT, 2) meet64_kernel(MeetArgs a) {
   }
   // ---- phase 2 -----------------------------------------------------------------------
   if (eng == 0) {
-    f_run<true>(s, a, st, b, h, Eb, Eb, potb, e, log2C);
+    f_run<true, XM>(s, a, st, b, h, Eb, Eb, potb, e, log2C);
   } else {
     st.Lnext = s.Lh;
-    b_run<true>(s, a, st, b, 0, h, Eb, potb, e, log2C);
+    b_run<true, XM>(s, a, st, b, 0, h, Eb, potb, e, log2C);
+  }
+  if (XM) {  // fused f1 epilogue: fixed-order engine reduction of the threads' Σ mu·x
+    double v = st.xacc;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((e & 31) == 0) s.xred[eng][e >> 5] = v;
+    named_bar(1 + eng, kNTE);
+    if (e == 0) {
+      double tot = 0.0;
+      for (int x = 0; x < kNW; ++x) tot += s.xred[eng][x];
+      a.xsum[2 * b + eng] = tot;
+    }
   }
 }
 
-std::atomic<uint64_t> g_meet_attr{0};
+std::atomic<uint64_t> g_meet_attr[3];
+template <int XM>
+cudaError_t launch_meet_x(const MeetArgs& a, cudaStream_t st) {
+  cudaError_t e = smem_optin_once(meet64_kernel<XM>, g_meet_attr[XM], (int)sizeof(MeetSmem));
+  if (e != cudaSuccess) return e;
+  meet64_kernel<XM><<<(unsigned)a.B, kNT, sizeof(MeetSmem), st>>>(a);
+  return cudaGetLastError();
+}
 }  // namespace
 
 bool meet_ok(int64_t C, const float* pot, const float* marg) {
@@ -539,10 +589,9 @@ bool meet_ok(int64_t C, const float* pot, const float* marg) {
 
 cudaError_t launch_meet(const MeetArgs& a, int64_t C, cudaStream_t st) {
   if (C != kC) return cudaErrorInvalidValue;
-  cudaError_t e = smem_optin_once(meet64_kernel, g_meet_attr, (int)sizeof(MeetSmem));
-  if (e != cudaSuccess) return e;
-  meet64_kernel<<<(unsigned)a.B, kNT, sizeof(MeetSmem), st>>>(a);
-  return cudaGetLastError();
+  if (a.xmode == 1) return launch_meet_x<1>(a, st);
+  if (a.xmode == 2) return launch_meet_x<2>(a, st);
+  return launch_meet_x<0>(a, st);
 }
 
 }  // namespace tsb

@@ -20,6 +20,11 @@ struct SmallArgs {
   float* marg;      // [B][N-1][C][C] or nullptr (logZ only)
   float* logz;      // [B]
   uint32_t* flags;  // [B] or nullptr
+  // fused f1 epilogue (fb_tiny only): xmode 1 = entropy H = A - Σ mu·l, 2 = expectation
+  // Σ mu·xr (terms with mu = 0 skipped); xout [B], NaN for flagged sequences
+  const float* xr;
+  int xmode;
+  float* xout;
 };
 size_t small_smem_bytes(int64_t N, int64_t C);
 bool small_fits(int64_t N, int64_t C);
@@ -85,6 +90,11 @@ struct MeetArgs {
   float* beta_hat;   // [B][N][C] backward node vectors, nodes h..E_b (scratch)
   float* mlag;       // [B][N]  forward lag bound per edge t < h (scratch)
   float* tshift;     // [B][N-1] natural-unit shift used for edge t (scratch)
+  // fused f1 epilogue: xmode 1 = Σ mu·l (entropy), 2 = Σ mu·xr (expectation);
+  // terms with mu = 0 skipped; per-engine fp64 partials xsum[2b + engine], fixed order
+  const float* xr;
+  int xmode;
+  double* xsum;
 };
 bool meet_ok(int64_t C, const float* pot, const float* marg);
 cudaError_t launch_meet(const MeetArgs& a, int64_t C, cudaStream_t st);
@@ -184,6 +194,8 @@ struct DistArgs {
 };
 int entropy_slices(const DistArgs& a);
 cudaError_t launch_entropy(DistArgs a, cudaStream_t st);
+// the final stage alone: out[b] from partial[b][0..S) (a fused marginal epilogue's partials)
+cudaError_t launch_entropy_final(const DistArgs& a, int S, cudaStream_t st);
 cudaError_t launch_score(const DistArgs& a, cudaStream_t st);
 cudaError_t launch_sample(const DistArgs& a, cudaStream_t st);
 

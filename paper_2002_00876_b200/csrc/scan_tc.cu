@@ -391,8 +391,13 @@ cudaError_t launch_np(const ScanArgs& a, cudaStream_t st) {
 }
 }  // namespace
 
+#ifndef TC_MIN_C
+#define TC_MIN_C 64
+#endif
+constexpr int kTcMinC = TC_MIN_C;  // tensor-core summaries for kTcMinC < C <= 128
+
 bool summary_tc_ok(const ScanArgs& a) {
-  return g_tc_summary.load() != 0 && a.C > 64 && a.C <= 128 && (a.C % 2) == 0 &&
+  return g_tc_summary.load() != 0 && a.C > kTcMinC && a.C <= 128 && (a.C % 2) == 0 &&
          (reinterpret_cast<uintptr_t>(a.pot) & 15) == 0;
 }
 

@@ -398,13 +398,17 @@ __device__ __forceinline__ void tiny_prepass(const float* __restrict__ raw, floa
 // t (fn[t]) and backward node t + 1 (bn[t+1]), then writes mu_t = u_t[i] EX[i][j] v_{t+1}[j] / Z_t
 // (exact log-space edge when Z_t / (U_t V_{t+1}) < 2^-30) to mg + t C^2.  Worker wi of
 // nworkers takes the edges qe = wi, wi + nworkers, ... of the centre-first order.
+// Fused f1 epilogue (xm != 0): the lane accumulates Σ mu·x over the elements it
+// writes (x = l from the staged raw tiles for xm = 1, x = xr[t] (global) for xm = 2; terms
+// with mu = 0 skipped), in a fixed order, into *xacc.
 template <int C, int TS = (C + 1) * tiny_rs(C)>
 __device__ __forceinline__ void tiny_marginals(const float* __restrict__ EXB, const float* __restrict__ raw,
                                                const float* __restrict__ Tm, const float* __restrict__ F,
                                                const float* __restrict__ HF, const float* __restrict__ G,
                                                const float* __restrict__ HG, uint64_t* fn, uint64_t* bn,
                                                int Eb, float* __restrict__ mg, int wi, int nworkers,
-                                               int lane) {
+                                               int lane, int xm = 0, const float* __restrict__ xr = nullptr,
+                                               double* xacc = nullptr) {
   constexpr int RS = tiny_rs(C), CC = C * C, Q4 = CC / 4;
   constexpr int NV = (Q4 + 31) / 32;
       for (int qe = wi; qe < Eb; qe += nworkers) {
@@ -449,12 +453,23 @@ __device__ __forceinline__ void tiny_marginals(const float* __restrict__ EXB, co
         float4* out = reinterpret_cast<float4*>(mg + (int64_t)t * CC);
         if (z >= kZGate * (u[C] * v[C])) {
           const float rz = __fdividef(1.f, z);
+          float xe = 0.f;
 #pragma unroll
           for (int m = 0; m < NV; ++m) {
             const int k = lane + 32 * m;
-            if (k < Q4)
-              out[k] = make_float4(val[m].x * rz, val[m].y * rz, val[m].z * rz, val[m].w * rz);
+            if (k < Q4) {
+              const float4 o = make_float4(val[m].x * rz, val[m].y * rz, val[m].z * rz, val[m].w * rz);
+              out[k] = o;
+              if (xm) {
+                const float4 x = reinterpret_cast<const float4*>((xm == 1 ? raw : xr) + (int64_t)t * CC)[k];
+                if (o.x != 0.f) xe = fmaf(o.x, x.x, xe);
+                if (o.y != 0.f) xe = fmaf(o.y, x.y, xe);
+                if (o.z != 0.f) xe = fmaf(o.z, x.z, xe);
+                if (o.w != 0.f) xe = fmaf(o.w, x.w, xe);
+              }
+            }
           }
+          if (xm) *xacc += (double)xe;
 #ifdef TS_PHASE_TIMING
           if (blockIdx.x == 0 && lane == 0 && t < 64) g_tiny_edge[t][2] = clock64();
 #endif
@@ -482,12 +497,18 @@ __device__ __forceinline__ void tiny_marginals(const float* __restrict__ EXB, co
           ss = warp_sum(ss);
           const float Lz = (mxl == neg_inf()) ? pos_inf() : mxl + lg2(ss);
           float* o = mg + (int64_t)t * CC;
+          float xe = 0.f;
           for (int k0 = 0; k0 < CC; k0 += 32) {
             const int k = k0 + lane, kk = k < CC ? k : 0;
             const int i = kk / C, j = kk - i * C;
             const float hi = __shfl_sync(0xffffffffu, hu, i), hj = __shfl_sync(0xffffffffu, hv, j);
-            if (k < CC) o[k] = ex2(hi + (rt[k] - Tt) * kLog2e + hj - Lz);
+            if (k < CC) {
+              const float mu = ex2(hi + (rt[k] - Tt) * kLog2e + hj - Lz);
+              o[k] = mu;
+              if (xm && mu != 0.f) xe = fmaf(mu, (xm == 1 ? raw : xr)[(int64_t)t * CC + k], xe);
+            }
           }
+          if (xm) *xacc += (double)xe;
         }
       }
 }
@@ -549,6 +570,7 @@ __device__ __noinline__ void tiny_body(const SmallArgs& a, const int64_t b, floa
     if (tid == 0) {
       a.logz[b] = qnan();
       if (a.flags) a.flags[b] = TS_F_BADLEN;
+      if (a.xmode) a.xout[b] = qnan();
     }
     return;
   }
@@ -566,6 +588,7 @@ __device__ __noinline__ void tiny_body(const SmallArgs& a, const int64_t b, floa
   TPHASE(2);
 
   const float ones0 = lane < C ? 1.f : (lane == C ? (float)C : 0.f);  // log-one start vector
+  double xacc = 0.0;  // fused f1 epilogue: this lane's Σ mu·x
   if (warp == kFwdWarp) {
     // ---- forward recursion, then logZ -------------------------------------------------
     const int kbf = tiny_sweep<true, C>(EXF, raw, Tm, F, HF, cf, fn, Eb, lane, ones0);
@@ -591,7 +614,8 @@ __device__ __noinline__ void tiny_body(const SmallArgs& a, const int64_t b, floa
   } else {
     // ---- marginals: centre edges first, one warp per edge, float4-wide -------------------
     if (mg) {
-      tiny_marginals<C>(EXB, raw, Tm, F, HF, G, HG, fn, bn, Eb, mg, wi, kWorkers, lane);
+      tiny_marginals<C>(EXB, raw, Tm, F, HF, G, HG, fn, bn, Eb, mg, wi, kWorkers, lane, a.xmode,
+                        a.xmode == 2 ? a.xr + b * E * CC : nullptr, &xacc);
       for (int64_t k = (int64_t)Eb * Q4 + (32 * wi + lane); k < E * Q4; k += 32 * kWorkers)
         reinterpret_cast<float4*>(mg)[k] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
@@ -605,6 +629,21 @@ __device__ __noinline__ void tiny_body(const SmallArgs& a, const int64_t b, floa
   if (mg && (fl & (TS_F_EMPTY | TS_F_NONFINITE)))
     for (int64_t k = tid; k < E * Q4; k += kTinyThreads)
       reinterpret_cast<float4*>(mg)[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (a.xmode) {  // fused f1 epilogue: fixed-order CTA reduction, H = A - Σ mu·l or Σ mu·r
+    __shared__ double xred[kTinyWarps];
+    double v = xacc;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) xred[warp] = v;
+    __syncthreads();
+    if (tid == 0) {
+      double tot = 0.0;
+      for (int w = 0; w < kTinyWarps; ++w) tot += xred[w];
+      const float lz = a.logz[b];
+      const bool bad = fl != 0u || !(lz > -INFINITY && lz < INFINITY);
+      a.xout[b] = bad ? qnan() : (float)(a.xmode == 1 ? (double)lz - tot : tot);
+    }
+  }
 }
 
 }  // namespace tsb

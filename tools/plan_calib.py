@@ -34,21 +34,24 @@ def time_call(fn, warmup, iters):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--iters", type=int, default=5)
+    ap.add_argument("--tc", type=int, default=3)
+    ap.add_argument("--chunks", default="0,E,32,64,128,256,512,1024")
     ap.add_argument("--shapes", default="4x4096x64,8x4096x64,16x2048x64,32x1024x64,64x512x64,4x16384x64,"
                     "4x4096x32,16x2048x32,4x4096x128,16x2048x128,32x1024x128,64x1024x128")
     args = ap.parse_args()
     dev = torch.device("cuda:0")
+    tsb.set_tc_summary(args.tc)
     for sh in args.shapes.split(","):
         B, N, C = [int(x) for x in sh.split("x")]
         E = N - 1
         pot = torch.empty((B, E, C, C), dtype=torch.float32, device=dev)
         tsgen.fill_torch(pot, 1234, s=10)
-        for L in [0, E, 32, 64, 128, 256, 512, 1024]:
+        for L in [E if x == "E" else int(x) for x in args.chunks.split(",")]:
             if L > E:
                 continue
             tsb.set_plan_chunk(L)
             ms = time_call(lambda: tsb.marginals(pot), 2, args.iters)
-            print(json.dumps({"B": B, "N": N, "C": C, "chunk": L, "kernel": tsb.last_kernel(),
+            print(json.dumps({"B": B, "N": N, "C": C, "chunk": L, "tc": args.tc, "kernel": tsb.last_kernel(),
                               "launches": tsb.last_launch_count(), "ms": round(ms, 4)}), flush=True)
         tsb.set_plan_chunk(0)
         del pot
