@@ -299,7 +299,7 @@ __global__ void __launch_bounds__(kTinyThreads, 1) fb_cscan_kernel(SmallArgs a) 
   const int Eb = (int)(len - 1);
   if (len < 0 || Eb < 2 * G) {  // BADLEN or too short to chunk: CTA 0 runs the whole sequence
     cluster_wait();
-    if (r == 0) tiny_body<C, false>(a, b, sm + Lay.tiny);
+    if (r == 0) tiny_body_fallback<C>(a, b, sm + Lay.tiny);
     return;
   }
   const int s = (int)((int64_t)r * Eb / G), L = (int)((int64_t)(r + 1) * Eb / G) - s;
@@ -342,7 +342,7 @@ __global__ void __launch_bounds__(kTinyThreads, 1) fb_cscan_kernel(SmallArgs a) 
   for (int q = 0; q < G; ++q)
     if (q != r) bad |= reinterpret_cast<const unsigned*>(rx + (int64_t)q * MB + TB)[2];
   if (bad) {  // a gate, NaN or +inf anywhere in the sequence: CTA 0 recomputes it exactly
-    if (r == 0) tiny_body<C, false>(a, b, sm + Lay.tiny);
+    if (r == 0) tiny_body_fallback<C>(a, b, sm + Lay.tiny);
     cluster_wait();
     return;
   }
@@ -404,7 +404,7 @@ size_t cscan_smem_bytes(int64_t N, int64_t C, int G) {
   return (size_t)cs_layout(N, (int)C, G).total * sizeof(float);
 }
 
-constexpr size_t kCscanSmemMax = 227 * 1024;
+constexpr size_t kCscanSmemMax = 227 * 1024 - 1024;  // dynamic; headroom for static shared
 
 bool cscan_fits(const SmallArgs& a, int G) {
   if (G != 2 && G != 4) return false;

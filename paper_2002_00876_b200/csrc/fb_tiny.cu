@@ -4,10 +4,10 @@
 
 namespace tsb {
 
-template <int C>
+template <int C, int XM>
 __global__ void __launch_bounds__(kTinyThreads, 1) fb_tiny_kernel(SmallArgs a) {
   extern __shared__ __align__(16) float sm[];
-  tiny_body<C, true>(a, blockIdx.x, sm);
+  tiny_body<C, true, XM>(a, blockIdx.x, sm);
 }
 
 size_t tiny_smem_bytes(int64_t N, int64_t C) {
@@ -23,18 +23,11 @@ bool tiny_fits(const SmallArgs& a) {
 }
 
 namespace {
-template <int C>
-cudaError_t launch_tiny_c(const SmallArgs& a, size_t smem, cudaStream_t st) {
+template <int C, int XM>
+cudaError_t launch_tiny_cx(const SmallArgs& a, size_t smem, cudaStream_t st) {
   static std::atomic<uint64_t> attr_mask{0};  // one-time attribute setup per device
-  int dev = 0;
-  cudaGetDevice(&dev);
-  const uint64_t bit = 1ull << (dev & 63);
-  if (!(attr_mask.load() & bit)) {
-    cudaError_t e = cudaFuncSetAttribute(fb_tiny_kernel<C>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    if (e != cudaSuccess) return e;
-    attr_mask.fetch_or(bit);
-  }
+  cudaError_t e = smem_optin_once(fb_tiny_kernel<C, XM>, attr_mask, 200 * 1024);
+  if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)a.B);
   cfg.blockDim = dim3(kTinyThreads);
@@ -45,7 +38,14 @@ cudaError_t launch_tiny_c(const SmallArgs& a, size_t smem, cudaStream_t st) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, fb_tiny_kernel<C>, a);
+  return cudaLaunchKernelEx(&cfg, fb_tiny_kernel<C, XM>, a);
+}
+// XM: the fused f1 epilogue variant (0 = plain marginals, the default instantiation)
+template <int C>
+cudaError_t launch_tiny_c(const SmallArgs& a, size_t smem, cudaStream_t st) {
+  if (a.xmode == 1) return launch_tiny_cx<C, 1>(a, smem, st);
+  if (a.xmode == 2) return launch_tiny_cx<C, 2>(a, smem, st);
+  return launch_tiny_cx<C, 0>(a, smem, st);
 }
 }  // namespace
 

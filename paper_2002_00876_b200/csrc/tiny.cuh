@@ -98,7 +98,7 @@ constexpr int kFlagSlot = 31;                      // V[n][31] = 1: node n has e
 __host__ __device__ constexpr int tiny_rs(int C) { return (C % 8 == 4) ? C : C + 4; }
 
 struct TinyLayout {
-  int64_t raw, exf, exb, T, F, HF, G, HG, cf, bar, total;  // float offsets
+  int64_t raw, exf, exb, T, F, HF, G, HG, cf, bar, xred, total;  // float offsets
 };
 
 // mbarriers: ld[E] (tile loaded), fn[N], bn[N] (node published)
@@ -116,7 +116,8 @@ __host__ __device__ inline TinyLayout tiny_layout(int64_t N, int C) {
   l.G = l.HF + N * 32;                 // [N][32] backward linear v_n (slot C: V_n, 31: flag)
   l.HG = l.G + N * 32;                 // [N][32] backward exact log2 v_n
   l.bar = (l.HG + N * 32 + 3) & ~(int64_t)3;
-  l.total = l.bar + 2 * (E + 2 * N) + 8;  // mbarriers (2 floats each) + flag words
+  l.xred = l.bar + 2 * (E + 2 * N) + 8;    // mbarriers (2 floats each) + flag words
+  l.total = l.xred + 2 * 32;               // fused f1 epilogue: per-warp fp64 partials
   return l;
 }
 
@@ -401,14 +402,15 @@ __device__ __forceinline__ void tiny_prepass(const float* __restrict__ raw, floa
 // Fused f1 epilogue (xm != 0): the lane accumulates Σ mu·x over the elements it
 // writes (x = l from the staged raw tiles for xm = 1, x = xr[t] (global) for xm = 2; terms
 // with mu = 0 skipped), in a fixed order, into *xacc.
-template <int C, int TS = (C + 1) * tiny_rs(C)>
+template <int C, int TS = (C + 1) * tiny_rs(C), int XM = 0>
 __device__ __forceinline__ void tiny_marginals(const float* __restrict__ EXB, const float* __restrict__ raw,
                                                const float* __restrict__ Tm, const float* __restrict__ F,
                                                const float* __restrict__ HF, const float* __restrict__ G,
                                                const float* __restrict__ HG, uint64_t* fn, uint64_t* bn,
                                                int Eb, float* __restrict__ mg, int wi, int nworkers,
-                                               int lane, int xm = 0, const float* __restrict__ xr = nullptr,
+                                               int lane, const float* __restrict__ xr = nullptr,
                                                double* xacc = nullptr) {
+  constexpr int xm = XM;
   constexpr int RS = tiny_rs(C), CC = C * C, Q4 = CC / 4;
   constexpr int NV = (Q4 + 31) / 32;
       for (int qe = wi; qe < Eb; qe += nworkers) {
@@ -517,8 +519,8 @@ __device__ __forceinline__ void tiny_marginals(const float* __restrict__ EXB, co
 // shared memory at `sm` (tiny_layout).  PROLOGUE: this call owns the PDL handshake
 // (launch_dependents, L2 prefetch, griddepcontrol.wait); the cluster scan's exact fallback
 // calls it with PROLOGUE = false after its own prologue.
-template <int C, bool PROLOGUE>
-__device__ __noinline__ void tiny_body(const SmallArgs& a, const int64_t b, float* __restrict__ sm) {
+template <int C, bool PROLOGUE, int XM = 0>
+__device__ __forceinline__ void tiny_body(const SmallArgs& a, const int64_t b, float* __restrict__ sm) {
   constexpr int CC = C * C, Q4 = CC / 4;
   const int64_t N = a.N, E = N - 1;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -570,7 +572,7 @@ __device__ __noinline__ void tiny_body(const SmallArgs& a, const int64_t b, floa
     if (tid == 0) {
       a.logz[b] = qnan();
       if (a.flags) a.flags[b] = TS_F_BADLEN;
-      if (a.xmode) a.xout[b] = qnan();
+      if (XM) a.xout[b] = qnan();
     }
     return;
   }
@@ -614,8 +616,9 @@ __device__ __noinline__ void tiny_body(const SmallArgs& a, const int64_t b, floa
   } else {
     // ---- marginals: centre edges first, one warp per edge, float4-wide -------------------
     if (mg) {
-      tiny_marginals<C>(EXB, raw, Tm, F, HF, G, HG, fn, bn, Eb, mg, wi, kWorkers, lane, a.xmode,
-                        a.xmode == 2 ? a.xr + b * E * CC : nullptr, &xacc);
+      tiny_marginals<C, (C + 1) * tiny_rs(C), XM>(EXB, raw, Tm, F, HF, G, HG, fn, bn, Eb, mg, wi,
+                                                  kWorkers, lane, XM == 2 ? a.xr + b * E * CC : nullptr,
+                                                  &xacc);
       for (int64_t k = (int64_t)Eb * Q4 + (32 * wi + lane); k < E * Q4; k += 32 * kWorkers)
         reinterpret_cast<float4*>(mg)[k] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
@@ -629,8 +632,8 @@ __device__ __noinline__ void tiny_body(const SmallArgs& a, const int64_t b, floa
   if (mg && (fl & (TS_F_EMPTY | TS_F_NONFINITE)))
     for (int64_t k = tid; k < E * Q4; k += kTinyThreads)
       reinterpret_cast<float4*>(mg)[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (a.xmode) {  // fused f1 epilogue: fixed-order CTA reduction, H = A - Σ mu·l or Σ mu·r
-    __shared__ double xred[kTinyWarps];
+  if (XM) {  // fused f1 epilogue: fixed-order CTA reduction, H = A - Σ mu·l or Σ mu·r
+    double* xred = reinterpret_cast<double*>(sm + Lay.xred);
     double v = xacc;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -641,9 +644,16 @@ __device__ __noinline__ void tiny_body(const SmallArgs& a, const int64_t b, floa
       for (int w = 0; w < kTinyWarps; ++w) tot += xred[w];
       const float lz = a.logz[b];
       const bool bad = fl != 0u || !(lz > -INFINITY && lz < INFINITY);
-      a.xout[b] = bad ? qnan() : (float)(a.xmode == 1 ? (double)lz - tot : tot);
+      a.xout[b] = bad ? qnan() : (float)(XM == 1 ? (double)lz - tot : tot);
     }
   }
+}
+
+// The cluster scan's exact fallback: one non-inlined copy of the body, so the cluster
+// kernel's hot path stays small (it measured instruction-fetch bound with the body inlined).
+template <int C>
+__device__ __noinline__ void tiny_body_fallback(const SmallArgs& a, const int64_t b, float* __restrict__ sm) {
+  tiny_body<C, false>(a, b, sm);
 }
 
 }  // namespace tsb

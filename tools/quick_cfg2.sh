@@ -1,0 +1,3 @@
+cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
+timeout 300 python bench.py --steps 2000 --warmup 50 --reps 3 --side "" --no-cpu-baseline --e2e-steps 20 > gpurun_out/q_bench.json 2> gpurun_out/q_bench.err
+timeout 900 python -m pytest tests/test_parity_gpu.py tests/test_tiny_gpu.py tests/test_dist_gpu.py tests/test_meet_gpu.py -q -x -p no:cacheprovider > gpurun_out/q_tests.log 2>&1; tail -3 gpurun_out/q_tests.log
