@@ -20,10 +20,13 @@ int main(int argc, char** argv) {
   ScanArgs a{};
   a.pot = pot; a.lengths = nullptr; a.B = NCTA; a.N = N; a.C = C; a.L = L; a.P = 1; a.Ppad = 1;
   a.nodes = 1; a.H = 0; a.mat = mat; a.off = off; a.ident = ident; a.cflag = cflag; a.wflags = wflags;
+  if (getenv("TC1")) set_tc_summary(1);
   for (int it = 0; it < 3; ++it) launch_summary_tc(a, 0);
   cudaDeviceSynchronize();
   static long long t[64][8];
+#ifdef TS_TC_TIMING
   cudaMemcpyFromSymbol(t, g_tc_t, sizeof(t));
+#endif
   printf("u: Await | Aready | issued | Dready | sum | Wready | Awritten | prodB(u)   (rel. to Await of u)\n");
   for (int u = 0; u < 20 && u < L; ++u) {
     printf("%2d:", u);
@@ -31,6 +34,13 @@ int main(int argc, char** argv) {
     if (u > 0) printf("   step=%lld", t[u][0] - t[u - 1][0]);
     printf("\n");
   }
+  static long long pp[64][6];
+#ifdef TS_TC_TIMING
+  cudaMemcpyFromSymbol(pp, g_tc_p, sizeof(pp));
+#endif
+  printf("producer warp 0 (rel. to MMA issuer t0 of the same u): staged | pass1 | Bfree | pass2\n");
+  for (int u = 0; u < 20 && u < L; ++u)
+    printf("%2d: %7lld %7lld %7lld %7lld | loopdone %7lld fenced %7lld\n", u, pp[u][0] - t[u][0], pp[u][1] - t[u][0], pp[u][2] - t[u][0], pp[u][3] - t[u][0], pp[u][4] - t[u][0], pp[u][5] - t[u][0]);
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
   cudaEventRecord(e0);
   for (int it = 0; it < 5; ++it) launch_summary_tc(a, 0);
