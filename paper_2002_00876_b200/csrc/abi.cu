@@ -99,13 +99,15 @@ int device_sms() {
 //            per edge, times ceil(B / #SMs) waves;
 //   chunked: C <= 64 (SIMT summaries, C^3 per edge): ~0.39 + 4.5e-5 B E ms (C = 64) and
 //            ~0.45 + 1.1e-5 B E ms (C = 32) with L = 64 (the best of 32..1024 in every shape);
+//            C <= 32 beyond the one-CTA kernels' shared memory: always chunked, L = 16 / 32
+//            (profiles/r2_ablations.jsonl X4: 5-8x faster than the serial sweeps at N >= 128);
 //            C = 128 (tensor-core summaries): best L = E / floor(#SMs / B), at least 128
 //            (one wave of chunk summaries; cfg5: 37 chunks of 1772 edges, 17.7 ms, vs 32
 //            chunks of 2048, 20.1 ms).
 // The serial plan wins for C = 64 once B >~ 30 (e.g. every per-rank shape of cfg3's batch
 // sharding: B = 256 / G); chunking pays for few long sequences (cfg5).
 int64_t auto_chunk(int64_t B, int64_t E, int64_t C, int sms) {
-  if (E < 64) return 0;
+  if (E < 64 && C > 32) return 0;
   const double waves = (double)((B + sms - 1) / sms);
   if (C > 64) {
     if (2 * B > sms) return 0;
@@ -113,9 +115,13 @@ int64_t auto_chunk(int64_t B, int64_t E, int64_t C, int sms) {
     const int64_t L = (E + per - 1) / per;
     return L < 128 ? 128 : L;
   }
+  if (C <= 32) {  // the generic serial sweeps cost 2.6-4.3 us per edge here: chunk from E >= 32
+    if (E < 32) return 0;
+    return E <= 1024 ? 16 : 32;  // X4 ablation (B16 C20 N 64..512): L = 16 best, 0.20-0.38 ms
+  }
   const bool meet = (C == 64);
   const double serial_ms = (meet ? 1.2e-3 : 2.6e-3) * (double)E * waves;
-  const double chunk_ms = (C > 32 ? 0.39 + 4.5e-5 * (double)(B * E) : 0.45 + 1.1e-5 * (double)(B * E));
+  const double chunk_ms = 0.39 + 4.5e-5 * (double)(B * E);
   return chunk_ms < serial_ms ? 64 : 0;
 }
 
