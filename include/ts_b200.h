@@ -309,10 +309,15 @@ TS_API ts_status ts_segment_finish(const ts_chain *local, int64_t edge_begin, in
                                    float *marg_or_null, float *logz, uint32_t *flags, void *ws,
                                    size_t ws_bytes, void *stream);
 
-/* Debug/testing plan knob (process-global): chunk length L of the time-chunked scan.
+/* Plan knob (process-global): chunk length L of the time-chunked scan.
  * 0 = automatic; 1 = the paper's pure Fig. 4 tree (every edge a leaf); >= N-1 = serial
- * sweep (no tree).  Results agree across plans within the parity tolerances (Viterbi:
- * bit-identical). */
+ * sweep (no tree).  Applies to the log semiring (logZ, marginals, f1) and to the max
+ * semiring (ts_viterbi, ts_logpartition / ts_marginals with TS_MAX; C <= 158): max-plus
+ * chunk summaries, a fixed-order combine of the boundary vectors, chunk-local forwards with
+ * first-index backpointers, end-label maps and chunk backtracks (the automatic plan keeps
+ * the serial sweep for Viterbi).  Results agree across plans within the parity tolerances
+ * (Viterbi: bit-identical on inputs whose partial path sums are exact, e.g. the dyadic
+ * generator). */
 TS_API void ts_set_plan_chunk(int64_t L);
 TS_API int64_t ts_get_plan_chunk(void);
 

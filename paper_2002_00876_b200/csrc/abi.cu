@@ -225,11 +225,28 @@ size_t stream_ws(const ts_chain* c, const Plan& pl, bool marg, void* ws, StreamW
   return cv.off;
 }
 
+// Chunk length of the single-GPU time-chunked Viterbi (vchunk.cu), 0 = the serial sweep.
+// Knob (ts_set_plan_chunk): 1 <= L < E forces chunks of L edges; auto: see below.
+int64_t vit_chunk(const ts_chain* c) {
+  const int64_t knob = g_plan_chunk.load();
+  const int64_t E = c->N - 1;
+  if (E < 2 || !vchunk_ok(c->C)) return 0;
+  if (knob > 0) return knob < E ? knob : 0;
+  return 0;  // auto: the serial sweep (vit2 / viterbi_fwd)
+}
+
 struct VitWs {
   uint8_t* bp = nullptr;
   int32_t* zend = nullptr;
   int32_t* path = nullptr;
   float* score = nullptr;
+  // chunked plan
+  int64_t L = 0, P = 0;
+  float* summ = nullptr;
+  float* din = nullptr;
+  int32_t* maps = nullptr;
+  int32_t* czend = nullptr;
+  int32_t* zglob = nullptr;
 };
 size_t vit_ws(const ts_chain* c, bool need_path, bool need_score, void* ws, VitWs* out) {
   Carve cv(ws);
@@ -239,6 +256,17 @@ size_t vit_ws(const ts_chain* c, bool need_path, bool need_score, void* ws, VitW
   w.zend = cv.take<int32_t>((size_t)B);
   if (need_path) w.path = cv.take<int32_t>((size_t)(B * N));
   if (need_score) w.score = cv.take<float>((size_t)B);
+  const int64_t L = vit_chunk(c);
+  if (L > 0) {
+    w.L = L;
+    w.P = (E + L - 1) / L;
+    w.summ = cv.take<float>((size_t)(B * w.P * C * C));
+    w.din = cv.take<float>((size_t)(B * w.P * C));
+    w.maps = cv.take<int32_t>((size_t)(B * w.P * C));
+    w.czend = cv.take<int32_t>((size_t)(B * w.P));
+    w.zglob = cv.take<int32_t>((size_t)B);
+    if (!w.path) w.path = cv.take<int32_t>((size_t)(B * N));  // the chunked backtrack's target
+  }
   if (out) *out = w;
   return cv.off;
 }
@@ -472,6 +500,37 @@ ts_status run_max(const ts_chain* c, int op, float* marg, float* logz, int32_t* 
   a.path = path ? path : w.path;
   a.marg = marg;
   a.logz = logz;
+  if (w.P > 0) {  // time-chunked max-plus scan (vchunk.cu)
+    VChunkArgs v{};
+    v.pot = c->pot;
+    v.lengths = c->lengths;
+    v.B = c->B;
+    v.N = c->N;
+    v.C = c->C;
+    v.L = w.L;
+    v.P = w.P;
+    v.summ = w.summ;
+    v.din = w.din;
+    v.bp = w.bp;
+    v.maps = w.maps;
+    v.zend = w.czend;
+    v.zglob = w.zglob;
+    v.score = a.score;
+    v.logz = logz;
+    v.flags = flags;
+    v.path = a.path;
+    const bool want_path = (path != nullptr) || (marg != nullptr);
+    int n = 0;
+    cudaError_t e = launch_vchunk(v, want_path, st, &n);
+    if (e == cudaSuccess && marg) {
+      e = launch_indicator(a, st);
+      ++n;
+    }
+    if (e != cudaSuccess) return cuda_status(e);
+    t_launches = n;
+    t_kernel = "vch_summary_kernel";
+    return TS_OK;
+  }
   int n = 0;
   ts_status r = cuda_status(launch_viterbi(a, st, &n, g_vsplit.load()));
   if (r == TS_OK) t_launches = n;

@@ -167,6 +167,8 @@ size_t vit_smem_bytes(int64_t C, int stages, int rows_per_stage);
 // C in {128, 256}); 1/2/4/8 = forced cluster size for C in {128, 256}.
 cudaError_t launch_viterbi(const VitArgs& a, cudaStream_t st, int* launches, int vsplit);
 cudaError_t launch_backtrack(const VitArgs& a, cudaStream_t st);
+// one-hot dA*/dl from a.path into a.marg (ts_marginals(TS_MAX)); no-op without marg
+cudaError_t launch_indicator(const VitArgs& a, cudaStream_t st);
 cudaError_t launch_vit1(const VitArgs& a, cudaStream_t st);
 // cluster column-split forward (viterbi2.cu)
 bool vit2_ok(const VitArgs& a);
@@ -263,6 +265,27 @@ struct VsegArgs {
   int32_t* zend;          // [B] this segment's end label
 };
 cudaError_t launch_vseg_summary(const VsegArgs& a, cudaStream_t st);
+
+// ---- single-GPU time-chunked Viterbi (vchunk.cu) -------------------------------------------
+struct VChunkArgs {
+  const float* pot;
+  const int32_t* lengths;
+  int64_t B, N, C;
+  int64_t L, P;        // chunk length, chunks per sequence (P = ceil((N-1) / L))
+  float* summ;         // [B P][C][C] chunk max-plus summaries
+  float* din;          // [B P][C] boundary vectors
+  uint8_t* bp;         // [B][N-1][C] backpointers
+  int32_t* maps;       // [B P][C] end label -> first-node label of the chunk
+  int32_t* zend;       // [B P] chunk end labels
+  int32_t* zglob;      // [B] final label
+  float* score;        // [B]
+  float* logz;         // [B] or nullptr (copy of the score)
+  uint32_t* flags;     // [B] or nullptr
+  int32_t* path;       // [B][N]
+};
+size_t vchunk_ws_floats(const VChunkArgs& a);
+bool vchunk_ok(int64_t C);
+cudaError_t launch_vchunk(const VChunkArgs& a, bool want_path, cudaStream_t st, int* launches);
 cudaError_t launch_vseg_combine(const VsegArgs& a, cudaStream_t st);
 cudaError_t launch_vseg_maps(const VsegArgs& a, cudaStream_t st);
 cudaError_t launch_vseg_endlabel(const VsegArgs& a, cudaStream_t st);

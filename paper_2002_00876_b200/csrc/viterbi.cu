@@ -336,6 +336,12 @@ cudaError_t launch_viterbi(const VitArgs& a, cudaStream_t st, int* launches, int
   return cudaSuccess;
 }
 
+cudaError_t launch_indicator(const VitArgs& a, cudaStream_t st) {
+  if (!(a.marg && a.N > 1)) return cudaSuccess;
+  indicator_kernel<<<dim3((unsigned)(a.N - 1), (unsigned)a.B), 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_backtrack(const VitArgs& a, cudaStream_t st) {
   cudaError_t e = set_smem(backtrack_kernel, 2);
   if (e != cudaSuccess) return e;
