@@ -120,10 +120,18 @@ TS_API ts_status ts_viterbi(const ts_chain *c, int32_t *path, float *score, uint
  * Reading R17: c->pot is [B][N-1][K][C][C] fp32; l[b][n][k-1][c1][c2] scores a
  * segment covering the k steps n -> n+k (1 <= k <= K <= 16) with label c2 after label c1
  * at node n; a labelled segmentation of nodes 0 .. len-1 scores the sum of its segments.
- * K = 1 is exactly the linear chain.  Segmental forward-backward (per-cell max, fp64
- * offsets): logz [B] out (required); marg (same layout as pot, 0 for parts that end beyond
- * the sequence) out or NULL; flags as ts_marginals.  C <= 256.
- * ws: ts_semimarkov_workspace_bytes(c, K) bytes, 256-byte aligned. */
+ * K = 1 is exactly the linear chain.  logz [B] out (required); marg (same layout as pot, 0
+ * for parts that end beyond the sequence) out or NULL; flags as ts_marginals.  C <= 256.
+ * Plans: the segmental forward-backward on one CTA per sequence (per-cell max, fp64
+ * offsets), or — when ts_set_plan_chunk asks for a chunk length, or automatically for long
+ * chains (N-1 >= 256) with C K <= 128 — the scan of §6(a) on the expanded-state
+ * chain of S = C K states (label, steps to the next boundary): the potentials are expanded
+ * to [B][N-1][S][S] in the workspace, every linear-chain plan runs on them (chunked scan
+ * with tensor-core summaries, Fig. 4 tree, serial sweeps), and the part marginals are
+ * gathered back; ts_semimarkov_viterbi likewise runs the max plans (serial, time-chunked)
+ * on the expanded chain, whose first-index order is reading R18's.
+ * ws: ts_semimarkov_workspace_bytes(c, K) bytes, 256-byte aligned (the expanded plan needs
+ * 2 B (N-1) S^2 floats plus the chain's own workspace). */
 TS_API size_t ts_semimarkov_workspace_bytes(const ts_chain *c, int64_t K);
 /* Semi-Markov Viterbi (the max semiring, over the segmentations of R17):
  * the best labelled segmentation, canonical by reading R18 (backpointers = the first

@@ -818,8 +818,48 @@ TS_API size_t ts_workspace_bytes(const ts_chain* c, int op, ts_semiring s) {
   return op_ws(c, op, s, nullptr, nullptr, nullptr);
 }
 
+// Semi-Markov plan (semi_expand.cu): the expanded-state chain (S = C K states) whenever the
+// plan knob asks for a chunk length, or automatically for long chains (E >= 256) with
+// S <= 128 (tensor-core chunk summaries); otherwise the segmental one-CTA kernels.
+bool semi_expanded(const ts_chain* c, int64_t K) {
+  const int64_t S = c->C * K, E = c->N - 1;
+  if (K < 1 || S > 256 || E < 1) return false;
+  if (g_plan_chunk.load() > 0) return true;
+  return S <= 128 && E >= 256;
+}
+ts_chain semi_xchain(const ts_chain* c, int64_t K, const float* xpot) {
+  ts_chain x = *c;
+  x.C = c->C * K;
+  x.pot = xpot;
+  return x;
+}
+// layout: xpot | xmarg (log) or xpath (max) | the chain workspace of the expanded call
+size_t semi_x_ws(const ts_chain* c, int64_t K, bool maxsemi, bool want_marg, void* ws,
+                 float** xpot, float** xmarg, int32_t** xpath, void** inner, size_t* inner_bytes) {
+  Carve cv(ws);
+  const int64_t S = c->C * K, E = c->N - 1 > 0 ? c->N - 1 : 1;
+  float* xp = cv.take<float>((size_t)(c->B * E * S * S));
+  float* xm = nullptr;
+  int32_t* xa = nullptr;
+  if (!maxsemi && want_marg) xm = cv.take<float>((size_t)(c->B * E * S * S));
+  if (maxsemi) xa = cv.take<int32_t>((size_t)(c->B * c->N));
+  const ts_chain x = semi_xchain(c, K, xp);
+  const size_t in_b = align_up(maxsemi ? op_ws(&x, TS_OP_VITERBI, TS_MAX, nullptr, nullptr, nullptr)
+                                       : op_ws(&x, want_marg ? TS_OP_MARG : TS_OP_LOGZ, TS_LOG,
+                                               nullptr, nullptr, nullptr));
+  void* in = cv.take<uint8_t>(in_b);
+  if (xpot) *xpot = xp;
+  if (xmarg) *xmarg = xm;
+  if (xpath) *xpath = xa;
+  if (inner) *inner = in;
+  if (inner_bytes) *inner_bytes = in_b;
+  return cv.off;
+}
+
 TS_API size_t ts_semimarkov_workspace_bytes(const ts_chain* c, int64_t K) {
   if (!chain_ok(c) || K < 1 || K > 16) return 0;
+  if (semi_expanded(c, K))
+    return semi_x_ws(c, K, false, true, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
   return semi_ws(c, K, nullptr, nullptr);
 }
 
@@ -829,6 +869,37 @@ TS_API ts_status ts_semimarkov(const ts_chain* c, int64_t K, float* marg, float*
       (marg && !aligned(marg, 4)) || (flags && !aligned(flags, 4)))
     return TS_E_INVALID;
   if (!device_ok()) return TS_E_UNSUPPORTED;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (semi_expanded(c, K)) {  // the expanded-state chain through the log plans (scan, tree)
+    float *xpot, *xmarg;
+    void* inner;
+    size_t inner_b;
+    const size_t need = semi_x_ws(c, K, false, marg != nullptr, ws, &xpot, &xmarg, nullptr,
+                                  &inner, &inner_b);
+    if (ws_bytes < need || !ws || !aligned(ws, kAlign)) return TS_E_WORKSPACE;
+    SemiExpandArgs x{};
+    x.pot = c->pot;
+    x.lengths = c->lengths;
+    x.B = c->B;
+    x.N = c->N;
+    x.C = c->C;
+    x.K = K;
+    x.xpot = xpot;
+    x.xmarg = xmarg;
+    x.marg = marg;
+    x.logz = logz;
+    cudaError_t e = launch_semi_expand(x, st);
+    if (e != cudaSuccess) return cuda_status(e);
+    const ts_chain xc = semi_xchain(c, K, xpot);
+    ts_status r = run_log(&xc, xmarg, logz, flags, inner, inner_b, st);
+    if (r != TS_OK) return r;
+    const int n = t_launches;
+    const char* kern = t_kernel;
+    if ((e = launch_semi_gather(x, st)) != cudaSuccess) return cuda_status(e);
+    t_launches = n + 2;
+    t_kernel = kern;
+    return TS_OK;
+  }
   SemiArgs a{};
   const size_t need = semi_ws(c, K, ws, &a);
   if (ws_bytes < need || !ws || !aligned(ws, kAlign)) return TS_E_WORKSPACE;
@@ -840,7 +911,7 @@ TS_API ts_status ts_semimarkov(const ts_chain* c, int64_t K, float* marg, float*
   a.marg = marg;
   a.logz = logz;
   a.flags = flags;
-  ts_status r = cuda_status(launch_semimarkov(a, static_cast<cudaStream_t>(stream)));
+  ts_status r = cuda_status(launch_semimarkov(a, st));
   if (r == TS_OK) {
     t_launches = 1;
     t_kernel = "semimarkov_kernel";
@@ -850,6 +921,8 @@ TS_API ts_status ts_semimarkov(const ts_chain* c, int64_t K, float* marg, float*
 
 TS_API size_t ts_semimarkov_viterbi_workspace_bytes(const ts_chain* c, int64_t K) {
   if (!chain_ok(c) || K < 1 || K > 16) return 0;
+  if (semi_expanded(c, K))
+    return semi_x_ws(c, K, true, false, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
   return align_up(sizeof(uint16_t) * (size_t)(c->B * c->N * c->C));
 }
 
@@ -859,6 +932,36 @@ TS_API ts_status ts_semimarkov_viterbi(const ts_chain* c, int64_t K, int32_t* se
       !aligned(score, 4) || (flags && !aligned(flags, 4)))
     return TS_E_INVALID;
   if (!device_ok()) return TS_E_UNSUPPORTED;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (semi_expanded(c, K)) {  // the expanded-state chain through the max plans (serial, chunked)
+    float* xpot;
+    int32_t* xpath;
+    void* inner;
+    size_t inner_b;
+    const size_t need = semi_x_ws(c, K, true, false, ws, &xpot, nullptr, &xpath, &inner, &inner_b);
+    if (ws_bytes < need || !ws || !aligned(ws, kAlign)) return TS_E_WORKSPACE;
+    SemiExpandArgs x{};
+    x.pot = c->pot;
+    x.lengths = c->lengths;
+    x.B = c->B;
+    x.N = c->N;
+    x.C = c->C;
+    x.K = K;
+    x.xpot = xpot;
+    x.xpath = xpath;
+    x.seg = seg;
+    cudaError_t e = launch_semi_expand(x, st);
+    if (e != cudaSuccess) return cuda_status(e);
+    const ts_chain xc = semi_xchain(c, K, xpot);
+    ts_status r = run_max(&xc, TS_OP_VITERBI, nullptr, nullptr, xpath, score, flags, inner, inner_b, st);
+    if (r != TS_OK) return r;
+    const int n = t_launches;
+    const char* kern = t_kernel;
+    if ((e = launch_semi_seg(x, st)) != cudaSuccess) return cuda_status(e);
+    t_launches = n + 2;
+    t_kernel = kern;
+    return TS_OK;
+  }
   const size_t need = ts_semimarkov_viterbi_workspace_bytes(c, K);
   if (ws_bytes < need || !ws || !aligned(ws, kAlign)) return TS_E_WORKSPACE;
   SemiVitArgs a{};
@@ -872,7 +975,7 @@ TS_API ts_status ts_semimarkov_viterbi(const ts_chain* c, int64_t K, int32_t* se
   a.score = score;
   a.flags = flags;
   a.bp = static_cast<uint16_t*>(ws);
-  ts_status r = cuda_status(launch_semimarkov_viterbi(a, static_cast<cudaStream_t>(stream)));
+  ts_status r = cuda_status(launch_semimarkov_viterbi(a, st));
   if (r == TS_OK) {
     t_launches = 1;
     t_kernel = "semimarkov_viterbi_kernel";

@@ -266,6 +266,22 @@ struct VsegArgs {
 };
 cudaError_t launch_vseg_summary(const VsegArgs& a, cudaStream_t st);
 
+// ---- semi-Markov through the expanded-state chain (semi_expand.cu) ------------------------
+struct SemiExpandArgs {
+  const float* pot;        // [B][N-1][K][C][C]
+  const int32_t* lengths;
+  int64_t B, N, C, K;
+  float* xpot;             // [B][N-1][S][S], S = C K (expanded chain potentials)
+  const float* xmarg;      // [B][N-1][S][S] expanded marginals (gather input)
+  float* marg;             // [B][N-1][K][C][C] or nullptr
+  float* logz;             // [B] (len = 1 fix-up) or nullptr
+  const int32_t* xpath;    // [B][N] expanded Viterbi path (seg input)
+  int32_t* seg;            // [B][N] semi-Markov Viterbi output
+};
+cudaError_t launch_semi_expand(const SemiExpandArgs& a, cudaStream_t st);
+cudaError_t launch_semi_gather(const SemiExpandArgs& a, cudaStream_t st);
+cudaError_t launch_semi_seg(const SemiExpandArgs& a, cudaStream_t st);
+
 // ---- single-GPU time-chunked Viterbi (vchunk.cu) -------------------------------------------
 struct VChunkArgs {
   const float* pot;
