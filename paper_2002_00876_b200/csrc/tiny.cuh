@@ -42,7 +42,7 @@ namespace tsb {
 #ifdef TS_PHASE_TIMING
 __device__ long long g_tiny_phase[1024][8];
 __device__ long long g_tiny_steps[2][64];
-__device__ long long g_tiny_wp[4][16][3];  // per warp: loaded, prepass done, marginals done
+__device__ long long g_tiny_wp[4][16][8];  // per warp phase stamps (prepass: 0 start, 3 max, 4 stores, 5 sums; 2 marginals done)
 __device__ long long g_tiny_edge[64][4];   // cta 0 per edge: waited, summed, stored
 #define TPHASE(k)                                                                       \
   do {                                                                                  \
@@ -409,11 +409,12 @@ __device__ __forceinline__ float fmax_nan_t(float a, float b) {
 // EXF's spare row = the row sums; the column sums (EXB's spare row) re-read EXF rows.
 // Shared memory sees ~46 wavefronts per 20 x 20 tile instead of ~100 (TMA write + raw read +
 // conflicted transposed stores + two sum re-reads).  NaN / +inf -> TS_F_NONFINITE.
+// ld: per-tile mbarriers of a TMA-staged raw area at `src` (nullptr: src is global memory).
 template <int C, int TS = (C + 1) * tiny_rs(C)>
 __device__ __forceinline__ void tiny_prepass_rows(const float* __restrict__ src, float* __restrict__ EXF,
                                                   float* __restrict__ EXB, float* __restrict__ Tm,
                                                   unsigned* sflag, int Eb, int warp, int nwarps,
-                                                  int lane) {
+                                                  int lane, uint64_t* ld = nullptr) {
   constexpr int RS = tiny_rs(C), CC = C * C, Q = C / 4;
   const bool act = lane < C;
   for (int t0 = warp; t0 < Eb; t0 += 2 * nwarps) {
@@ -423,12 +424,14 @@ __device__ __forceinline__ void tiny_prepass_rows(const float* __restrict__ src,
 #pragma unroll
     for (int n = 0; n < 2; ++n) {
       const int t = n ? t1 : t0;
+      if (ld && n < nt) mbar_wait(&ld[t], 0);
 #pragma unroll
       for (int q = 0; q < Q; ++q)
         v[n][q] = (act && n < nt) ? reinterpret_cast<const float4*>(src + (int64_t)t * CC + lane * C)[q]
                                   : make_float4(neg_inf(), neg_inf(), neg_inf(), neg_inf());
     }
     float mx[2], mn[2];
+    TWARP(0);
 #pragma unroll
     for (int n = 0; n < 2; ++n) {
       float m = neg_inf();
@@ -447,6 +450,7 @@ __device__ __forceinline__ void tiny_prepass_rows(const float* __restrict__ src,
                      ((nt > 1) & ((mx[1] != mx[1]) | (mx[1] == pos_inf())));
     (void)mn;
     if (bad && lane == 0) atomicOr(sflag, (unsigned)TS_F_NONFINITE);
+    TWARP(3);
 #pragma unroll
     for (int n = 0; n < 2; ++n) {
       if (n < nt) {
@@ -476,6 +480,7 @@ __device__ __forceinline__ void tiny_prepass_rows(const float* __restrict__ src,
       }
     }
     __syncwarp();
+    TWARP(4);
     if (act) {
 #pragma unroll
       for (int n = 0; n < 2; ++n) {
@@ -495,6 +500,7 @@ __device__ __forceinline__ void tiny_prepass_rows(const float* __restrict__ src,
         }
       }
     }
+    TWARP(5);
   }
 }
 
@@ -683,13 +689,20 @@ __device__ __forceinline__ void tiny_body(const SmallArgs& a, const int64_t b, f
   const float* src = a.pot + b * E * CC;
   // each warp bulk-copies the tiles it preps
   const int wi = worker_index(warp);
-#ifdef TINY_TMA_PREPASS
+#if defined(TINY_TMA_PREPASS)  // (variant: TMA staging, float4-per-lane prepass)
   if (lane == 0)
     for (int t = warp; t < Eb; t += kTinyWarps)
       bulk_load(raw + (int64_t)t * CC, src + (int64_t)t * CC, (uint32_t)(CC * 4), &ld[t]);
   TPHASE(0);
   tiny_prepass<C>(raw, EXF, EXB, Tm, ld, sflag, Eb, warp, kTinyWarps, lane);
-#else
+#elif defined(TINY_TMA_ROWS)  // (variant: TMA staging, row-per-lane reads; faster eager, 6.22
+                              // vs 5.97 us/step in the bench's graph)
+  if (lane == 0)
+    for (int t = warp; t < Eb; t += kTinyWarps)
+      bulk_load(raw + (int64_t)t * CC, src + (int64_t)t * CC, (uint32_t)(CC * 4), &ld[t]);
+  TPHASE(0);
+  tiny_prepass_rows<C>(raw, EXF, EXB, Tm, sflag, Eb, warp, kTinyWarps, lane, ld);
+#else  // default: row-per-lane straight from L2 (the PDL prologue prefetched the tiles)
   TPHASE(0);
   tiny_prepass_rows<C>(src, EXF, EXB, Tm, sflag, Eb, warp, kTinyWarps, lane);
   raw = const_cast<float*>(src);  // the exact (careful / gated) paths read the raw tiles here

@@ -26,11 +26,11 @@ int main(int argc, char** argv) {
     for (int k = 1; k < 7; ++k) printf(" %s=%lld", nm[k], ph[c][k] - ph[c][0]);
     printf("\n");
   }
-  static long long wp[4][16][3];
+  static long long wp[4][16][8];
   cudaMemcpyFromSymbol(wp, g_tiny_wp, sizeof(wp));
   for (int w = 0; w < 16; ++w)
-    printf("cta0 warp %2d: loaded=%lld prepass=%lld marg=%lld\n", w, wp[0][w][0] - ph[0][0],
-           wp[0][w][1] - ph[0][0], wp[0][w][2] - ph[0][0]);
+    printf("cta0 warp %2d: start=%lld maxed=%lld stored=%lld summed=%lld marg=%lld\n", w, wp[0][w][0] - ph[0][0],
+           wp[0][w][3] - ph[0][0], wp[0][w][4] - ph[0][0], wp[0][w][5] - ph[0][0], wp[0][w][2] - ph[0][0]);
   static long long ed[64][4];
   cudaMemcpyFromSymbol(ed, g_tiny_edge, sizeof(ed));
   for (int t = 0; t < E && t < 64; ++t)
