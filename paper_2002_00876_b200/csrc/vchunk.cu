@@ -115,6 +115,110 @@ __global__ void __launch_bounds__(256) vch_summary_kernel(VChunkArgs a) {
       if (m0 + r < C) a.summ[(s * C + m0 + r) * C + tid] = dl[buf * kVcR * NT + r * NT + tid];
 }
 
+// Register-blocked max-plus chunk summary for C % 16 == 0 (C <= 128): one CTA per chunk holds
+// the running product S = X_0 (x) ... (x) X_{t-1} (C x C, row-major in shared memory) and
+// multiplies it by the next tile, S'[m][j] = max_i S[m][i] + X[i][j]; thread (tr, tc) owns the
+// 8 x 8 output block rows 8 tr.., columns 8 tc.. (T = C / 8 row and column groups, T^2 threads).
+// Tiles are staged pair-interleaved, XP[i/2][j] = (X[i][j], X[i+1][j]), so that one packed
+// FADD2 forms the two terms of an i-pair and one FMNMX3.NaN folds both into the running max:
+// one instruction per term, NaN / +inf propagate into the summary (the combine flags them).
+// The next tile is loaded into registers while the current one is multiplied.
+__device__ __forceinline__ uint64_t add_f32x2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ float max3_nan(float a, float b, float c) {
+  float r;
+  asm("max.NaN.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
+template <int C>
+__global__ void __launch_bounds__((C / 8) * (C / 8), 1) vch_summary_mm_kernel(VChunkArgs a) {
+  constexpr int T = C / 8, NT = T * T, CC = C * C;
+  constexpr int PER = CC / NT;      // tile elements loaded per thread per step (64 at C = 128)
+  constexpr int GRP = PER / 8;      // (row pair, 4 columns) groups per thread
+  extern __shared__ __align__(16) float sm[];
+  float* S = sm;                    // [C][C]
+  float2* XP = reinterpret_cast<float2*>(sm + CC);  // [2][C/2][C]
+  const int64_t E = a.N - 1;
+  const int64_t s = blockIdx.x;
+  const Chunk ch = chunk_of(a, s);
+  const int tid = threadIdx.x, tr = tid / T, tc = tid - (tid / T) * T;
+  const float* potc = a.pot + (ch.b * E + ch.t0) * (int64_t)CC;
+  // identity start
+  for (int q = tid; q < CC; q += NT) S[q] = ((q / C) == (q % C)) ? 0.f : neg_inf();
+  // group g of this thread: row pair rp = (tid + NT g) / (C / 4), column quad cq
+  float4 nx[GRP][2];
+  auto load = [&](int64_t t) {
+    const float* tile = potc + t * CC;
+#pragma unroll
+    for (int g = 0; g < GRP; ++g) {
+      const int idx = tid + NT * g, rp = idx / (C / 4), cq = idx - rp * (C / 4);
+      nx[g][0] = *reinterpret_cast<const float4*>(tile + (2 * rp) * C + 4 * cq);
+      nx[g][1] = *reinterpret_cast<const float4*>(tile + (2 * rp + 1) * C + 4 * cq);
+    }
+  };
+  auto store = [&](int buf) {
+    float2* xp = XP + buf * (C / 2) * C;
+#pragma unroll
+    for (int g = 0; g < GRP; ++g) {
+      const int idx = tid + NT * g, rp = idx / (C / 4), cq = idx - rp * (C / 4);
+      float4* dst = reinterpret_cast<float4*>(xp + rp * C + 4 * cq);
+      dst[0] = make_float4(nx[g][0].x, nx[g][1].x, nx[g][0].y, nx[g][1].y);
+      dst[1] = make_float4(nx[g][0].z, nx[g][1].z, nx[g][0].w, nx[g][1].w);
+    }
+  };
+  if (ch.n > 0) {
+    load(0);
+    store(0);
+  }
+  for (int64_t t = 0; t < ch.n; ++t) {
+    __syncthreads();  // S and XP[t & 1] ready
+    if (t + 1 < ch.n) load(t + 1);
+    const float2* xp = XP + (t & 1) * (C / 2) * C + 8 * tc;
+    const float* srow = S + (8 * tr) * C;
+    float acc[8][8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) acc[r][c] = neg_inf();
+#pragma unroll 2
+    for (int ip = 0; ip < C / 2; ++ip) {
+      uint64_t av[8], bv[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) av[r] = *reinterpret_cast<const uint64_t*>(srow + r * C + 2 * ip);
+#pragma unroll
+      for (int c = 0; c < 8; c += 2) {
+        const float4 q = *reinterpret_cast<const float4*>(xp + ip * C + c);
+        bv[c] = (uint64_t)__float_as_uint(q.x) | ((uint64_t)__float_as_uint(q.y) << 32);
+        bv[c + 1] = (uint64_t)__float_as_uint(q.z) | ((uint64_t)__float_as_uint(q.w) << 32);
+      }
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const uint64_t sum = add_f32x2(av[r], bv[c]);
+          acc[r][c] = max3_nan(acc[r][c], __uint_as_float((uint32_t)sum),
+                               __uint_as_float((uint32_t)(sum >> 32)));
+        }
+    }
+    __syncthreads();  // every read of S and XP[t & 1] done
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      float4* d = reinterpret_cast<float4*>(S + (8 * tr + r) * C + 8 * tc);
+      d[0] = make_float4(acc[r][0], acc[r][1], acc[r][2], acc[r][3]);
+      d[1] = make_float4(acc[r][4], acc[r][5], acc[r][6], acc[r][7]);
+    }
+    if (t + 1 < ch.n) store((int)((t + 1) & 1));
+  }
+  __syncthreads();
+  float* out = a.summ + s * (int64_t)CC;
+  for (int q = tid; q < CC / 4; q += NT)
+    reinterpret_cast<float4*>(out)[q] = reinterpret_cast<const float4*>(S)[q];
+}
+
 // One CTA (256 threads) per sequence: delta_in of every chunk, A*, z_E, flags.
 __global__ void __launch_bounds__(256) vch_combine_kernel(VChunkArgs a) {
   __shared__ float v[2][256];
@@ -317,8 +421,12 @@ cudaError_t optin(K kern, std::atomic<uint64_t>& mask, size_t smem) {
   if (smem <= 48 * 1024) return cudaSuccess;
   return smem_optin_once(kern, mask, (int)smem);
 }
-std::atomic<uint64_t> g_attr_sum{0}, g_attr_fwd{0};
+std::atomic<uint64_t> g_attr_sum{0}, g_attr_fwd{0}, g_attr_mm[3];
+std::atomic<int> g_vch_mm{1};
+bool vch_mm_enabled() { return g_vch_mm.load() != 0; }
 }  // namespace
+
+void set_vchunk_mm(int enable) { g_vch_mm.store(enable ? 1 : 0); }
 
 size_t vchunk_ws_floats(const VChunkArgs& a) {
   return (size_t)(a.B * a.P) * (size_t)(a.C * a.C + a.C);
@@ -331,9 +439,29 @@ cudaError_t launch_vchunk(const VChunkArgs& a, bool want_path, cudaStream_t st, 
   const int NT = ((C + 31) / 32) * 32;
   const unsigned nseg = (unsigned)(a.B * a.P);
   cudaError_t e;
-  const size_t s_sum = vch_smem(C, 2 * kVcR * NT);
-  if ((e = optin(vch_summary_kernel, g_attr_sum, s_sum)) != cudaSuccess) return e;
-  vch_summary_kernel<<<dim3(nseg, (unsigned)((C + kVcR - 1) / kVcR)), NT, s_sum, st>>>(a);
+  const bool mm = (C == 128 || C == 64 || C == 32) && vch_mm_enabled() &&
+                  (reinterpret_cast<uintptr_t>(a.pot) & 15) == 0;
+  if (mm) {  // register-blocked max-plus products (FADD2 + FMNMX3)
+    const size_t s_mm = (size_t)3 * C * C * sizeof(float);
+    switch (C) {
+      case 128:
+        if ((e = optin(vch_summary_mm_kernel<128>, g_attr_mm[0], s_mm)) != cudaSuccess) return e;
+        vch_summary_mm_kernel<128><<<nseg, 256, s_mm, st>>>(a);
+        break;
+      case 64:
+        if ((e = optin(vch_summary_mm_kernel<64>, g_attr_mm[1], s_mm)) != cudaSuccess) return e;
+        vch_summary_mm_kernel<64><<<nseg, 64, s_mm, st>>>(a);
+        break;
+      default:
+        if ((e = optin(vch_summary_mm_kernel<32>, g_attr_mm[2], s_mm)) != cudaSuccess) return e;
+        vch_summary_mm_kernel<32><<<nseg, 16, s_mm, st>>>(a);
+        break;
+    }
+  } else {
+    const size_t s_sum = vch_smem(C, 2 * kVcR * NT);
+    if ((e = optin(vch_summary_kernel, g_attr_sum, s_sum)) != cudaSuccess) return e;
+    vch_summary_kernel<<<dim3(nseg, (unsigned)((C + kVcR - 1) / kVcR)), NT, s_sum, st>>>(a);
+  }
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   vch_combine_kernel<<<(unsigned)a.B, 256, 0, st>>>(a);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
