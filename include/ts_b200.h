@@ -357,6 +357,13 @@ TS_API void ts_set_wide_ring(int enable);
  * backward sweep kernels.  Results agree within the parity tolerances. */
 TS_API void ts_set_meet(int enable);
 
+/* Debug/testing knob (process-global) for the time-chunked Viterbi (ts_set_plan_chunk, and
+ * the automatic choice for long chains with C in {32, 64, 128}): 1 (default) = chunk
+ * summaries by the register-blocked max-plus product kernel where C in {32, 64, 128} and
+ * the potentials are 16-byte aligned; 0 = the row-chain summary kernel for every C (the
+ * automatic plan then keeps the serial sweep).  Results are bit-identical. */
+TS_API void ts_set_vchunk_mm(int enable);
+
 /* Debug/testing knob (process-global) for the Viterbi forward with C in {128, 256}:
  * 0 (default) = automatic cluster column split (the largest G in {1,2,4,8} with B*G CTAs
  * fitting the SMs, C/G >= 32); G in {1,2,4,8} = forced cluster size; -1 = the

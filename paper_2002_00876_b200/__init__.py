@@ -489,6 +489,12 @@ def set_meet(enable: bool) -> None:
     _lib.load().ts_set_meet(1 if enable else 0)
 
 
+def set_vchunk_mm(enable: bool) -> None:
+    """Debug knob: register-blocked max-plus chunk summaries of the chunked Viterbi for
+    C in {32, 64, 128} (default on; off = row-chain summaries, auto plan serial)."""
+    _lib.load().ts_set_vchunk_mm(1 if enable else 0)
+
+
 def set_viterbi_split(G: int) -> None:
     """Debug knob: Viterbi C in {128,256} cluster size (0 auto, 1/2/4/8 forced, -1 legacy)."""
     _lib.load().ts_set_viterbi_split(int(G))

@@ -226,13 +226,26 @@ size_t stream_ws(const ts_chain* c, const Plan& pl, bool marg, void* ws, StreamW
 }
 
 // Chunk length of the single-GPU time-chunked Viterbi (vchunk.cu), 0 = the serial sweep.
-// Knob (ts_set_plan_chunk): 1 <= L < E forces chunks of L edges; auto: see below.
+// Knob (ts_set_plan_chunk): 1 <= L < E forces chunks of L edges.  Auto (calibrated,
+// tools/vchunk_calib.py -> profiles/r2_vchunk_calib.jsonl): the serial sweeps cost ~1.5 us
+// per edge whatever B (one dependent step per edge: vit2 for C = 128, viterbi_fwd below);
+// the chunked scan with the register-blocked summaries (C in {32, 64, 128}) costs, once its
+// chunks fill the GPU, K(C) us per (sequence x edge) — 0.145 (C = 128, one 256-thread CTA
+// per SM), 0.020 (C = 64, four per SM), 0.007 (C = 32) — so it is chosen when
+// B K(C) < 0.7 x 1.5 us and the chains are long (E >= 256), with enough chunks per sequence
+// for one wave of NSEG(C) = #SMs x {1, 4, 8} CTAs.
 int64_t vit_chunk(const ts_chain* c) {
   const int64_t knob = g_plan_chunk.load();
-  const int64_t E = c->N - 1;
-  if (E < 2 || !vchunk_ok(c->C)) return 0;
+  const int64_t B = c->B, C = c->C, E = c->N - 1;
+  if (E < 2 || !vchunk_ok(C)) return 0;
   if (knob > 0) return knob < E ? knob : 0;
-  return 0;  // auto: the serial sweep (vit2 / viterbi_fwd)
+  if (E < 256 || !vchunk_mm(C) || B < 1 || (reinterpret_cast<uintptr_t>(c->pot) & 15) != 0) return 0;
+  const double K = C == 128 ? 0.145 : C == 64 ? 0.020 : 0.007;
+  if ((double)B * K >= 0.7 * 1.5) return 0;
+  const int64_t nseg = (int64_t)device_sms() * (C == 128 ? 1 : C == 64 ? 4 : 8);
+  const int64_t per = nseg / B;
+  if (per < 2) return 0;
+  return (E + per - 1) / per;
 }
 
 struct VitWs {
@@ -528,7 +541,7 @@ ts_status run_max(const ts_chain* c, int op, float* marg, float* logz, int32_t* 
     }
     if (e != cudaSuccess) return cuda_status(e);
     t_launches = n;
-    t_kernel = "vch_summary_kernel";
+    t_kernel = vchunk_mm(c->C) ? "vch_summary_mm_kernel" : "vch_summary_kernel";
     return TS_OK;
   }
   int n = 0;
@@ -1680,6 +1693,7 @@ TS_API ts_status ts_segment_finish(const ts_chain* local, int64_t edge_begin, in
 }
 
 TS_API void ts_set_meet(int enable) { g_meet.store(enable ? 1 : 0); }
+TS_API void ts_set_vchunk_mm(int enable) { set_vchunk_mm(enable); }
 TS_API void ts_set_viterbi_split(int G) {
   g_vsplit.store((G == -1 || G == 1 || G == 2 || G == 4 || G == 8) ? G : 0);
 }

@@ -303,6 +303,7 @@ size_t vchunk_ws_floats(const VChunkArgs& a);
 bool vchunk_ok(int64_t C);
 cudaError_t launch_vchunk(const VChunkArgs& a, bool want_path, cudaStream_t st, int* launches);
 void set_vchunk_mm(int enable);  // debug: 0 = row-chain summaries for every C
+bool vchunk_mm(int64_t C);        // the register-blocked summary kernel serves this C
 cudaError_t launch_vseg_combine(const VsegArgs& a, cudaStream_t st);
 cudaError_t launch_vseg_maps(const VsegArgs& a, cudaStream_t st);
 cudaError_t launch_vseg_endlabel(const VsegArgs& a, cudaStream_t st);

@@ -117,8 +117,9 @@ __global__ void __launch_bounds__(256) vch_summary_kernel(VChunkArgs a) {
 
 // Register-blocked max-plus chunk summary for C % 16 == 0 (C <= 128): one CTA per chunk holds
 // the running product S = X_0 (x) ... (x) X_{t-1} (C x C, row-major in shared memory) and
-// multiplies it by the next tile, S'[m][j] = max_i S[m][i] + X[i][j]; thread (tr, tc) owns the
-// 8 x 8 output block rows 8 tr.., columns 8 tc.. (T = C / 8 row and column groups, T^2 threads).
+// multiplies it by the next tile, S'[m][j] = max_i S[m][i] + X[i][j]; thread (tr, tc) owns an
+// 8 x 8 output block, strided so that shared-memory reads are conflict-free (T = C / 8, T^2
+// threads; S rows padded by 4 floats).
 // Tiles are staged pair-interleaved, XP[i/2][j] = (X[i][j], X[i+1][j]), so that one packed
 // FADD2 forms the two terms of an i-pair and one FMNMX3.NaN folds both into the running max:
 // one instruction per term, NaN / +inf propagate into the summary (the combine flags them).
@@ -137,18 +138,19 @@ __device__ __forceinline__ float max3_nan(float a, float b, float c) {
 template <int C>
 __global__ void __launch_bounds__((C / 8) * (C / 8), 1) vch_summary_mm_kernel(VChunkArgs a) {
   constexpr int T = C / 8, NT = T * T, CC = C * C;
+  constexpr int SP = C + 4;         // padded S row: the warp's T-row groups land on distinct banks
   constexpr int PER = CC / NT;      // tile elements loaded per thread per step (64 at C = 128)
   constexpr int GRP = PER / 8;      // (row pair, 4 columns) groups per thread
   extern __shared__ __align__(16) float sm[];
-  float* S = sm;                    // [C][C]
-  float2* XP = reinterpret_cast<float2*>(sm + CC);  // [2][C/2][C]
+  float* S = sm;                    // [C][SP]
+  float2* XP = reinterpret_cast<float2*>(sm + C * SP);  // [2][C/2][C]
   const int64_t E = a.N - 1;
   const int64_t s = blockIdx.x;
   const Chunk ch = chunk_of(a, s);
   const int tid = threadIdx.x, tr = tid / T, tc = tid - (tid / T) * T;
   const float* potc = a.pot + (ch.b * E + ch.t0) * (int64_t)CC;
   // identity start
-  for (int q = tid; q < CC; q += NT) S[q] = ((q / C) == (q % C)) ? 0.f : neg_inf();
+  for (int q = tid; q < CC; q += NT) S[(q / C) * SP + q % C] = ((q / C) == (q % C)) ? 0.f : neg_inf();
   // group g of this thread: row pair rp = (tid + NT g) / (C / 4), column quad cq
   float4 nx[GRP][2];
   auto load = [&](int64_t t) {
@@ -174,11 +176,14 @@ __global__ void __launch_bounds__((C / 8) * (C / 8), 1) vch_summary_mm_kernel(VC
     load(0);
     store(0);
   }
+  // thread (tr, tc) owns rows tr + T r and columns 2 tc + 2 T m + e (r < 8, m < 4, e < 2):
+  // a warp's column loads are T contiguous 16-byte float4s, its row loads 32 / T distinct
+  // padded rows in distinct banks
   for (int64_t t = 0; t < ch.n; ++t) {
     __syncthreads();  // S and XP[t & 1] ready
     if (t + 1 < ch.n) load(t + 1);
-    const float2* xp = XP + (t & 1) * (C / 2) * C + 8 * tc;
-    const float* srow = S + (8 * tr) * C;
+    const float2* xp = XP + (t & 1) * (C / 2) * C + 2 * tc;
+    const float* srow = S + tr * SP;
     float acc[8][8];
 #pragma unroll
     for (int r = 0; r < 8; ++r)
@@ -188,12 +193,13 @@ __global__ void __launch_bounds__((C / 8) * (C / 8), 1) vch_summary_mm_kernel(VC
     for (int ip = 0; ip < C / 2; ++ip) {
       uint64_t av[8], bv[8];
 #pragma unroll
-      for (int r = 0; r < 8; ++r) av[r] = *reinterpret_cast<const uint64_t*>(srow + r * C + 2 * ip);
+      for (int r = 0; r < 8; ++r)
+        av[r] = *reinterpret_cast<const uint64_t*>(srow + (T * r) * SP + 2 * ip);
 #pragma unroll
-      for (int c = 0; c < 8; c += 2) {
-        const float4 q = *reinterpret_cast<const float4*>(xp + ip * C + c);
-        bv[c] = (uint64_t)__float_as_uint(q.x) | ((uint64_t)__float_as_uint(q.y) << 32);
-        bv[c + 1] = (uint64_t)__float_as_uint(q.z) | ((uint64_t)__float_as_uint(q.w) << 32);
+      for (int m = 0; m < 4; ++m) {
+        const float4 q = *reinterpret_cast<const float4*>(xp + ip * C + 2 * T * m);
+        bv[2 * m] = (uint64_t)__float_as_uint(q.x) | ((uint64_t)__float_as_uint(q.y) << 32);
+        bv[2 * m + 1] = (uint64_t)__float_as_uint(q.z) | ((uint64_t)__float_as_uint(q.w) << 32);
       }
 #pragma unroll
       for (int r = 0; r < 8; ++r)
@@ -206,17 +212,19 @@ __global__ void __launch_bounds__((C / 8) * (C / 8), 1) vch_summary_mm_kernel(VC
     }
     __syncthreads();  // every read of S and XP[t & 1] done
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      float4* d = reinterpret_cast<float4*>(S + (8 * tr + r) * C + 8 * tc);
-      d[0] = make_float4(acc[r][0], acc[r][1], acc[r][2], acc[r][3]);
-      d[1] = make_float4(acc[r][4], acc[r][5], acc[r][6], acc[r][7]);
-    }
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+        *reinterpret_cast<float2*>(S + (tr + T * r) * SP + 2 * tc + 2 * T * m) =
+            make_float2(acc[r][2 * m], acc[r][2 * m + 1]);
     if (t + 1 < ch.n) store((int)((t + 1) & 1));
   }
   __syncthreads();
   float* out = a.summ + s * (int64_t)CC;
-  for (int q = tid; q < CC / 4; q += NT)
-    reinterpret_cast<float4*>(out)[q] = reinterpret_cast<const float4*>(S)[q];
+  for (int q = tid; q < CC / 4; q += NT) {
+    const int i = (4 * q) / C, j = 4 * q - i * C;
+    reinterpret_cast<float4*>(out)[q] = *reinterpret_cast<const float4*>(S + i * SP + j);
+  }
 }
 
 // One CTA (256 threads) per sequence: delta_in of every chunk, A*, z_E, flags.
@@ -434,15 +442,16 @@ size_t vchunk_ws_floats(const VChunkArgs& a) {
 
 bool vchunk_ok(int64_t C) { return C >= 1 && C <= 256 && vch_smem((int)C, 2 * kVcR * 256) <= 200 * 1024; }
 
+bool vchunk_mm(int64_t C) { return (C == 128 || C == 64 || C == 32) && vch_mm_enabled(); }
+
 cudaError_t launch_vchunk(const VChunkArgs& a, bool want_path, cudaStream_t st, int* launches) {
   const int C = (int)a.C;
   const int NT = ((C + 31) / 32) * 32;
   const unsigned nseg = (unsigned)(a.B * a.P);
   cudaError_t e;
-  const bool mm = (C == 128 || C == 64 || C == 32) && vch_mm_enabled() &&
-                  (reinterpret_cast<uintptr_t>(a.pot) & 15) == 0;
+  const bool mm = vchunk_mm(C) && (reinterpret_cast<uintptr_t>(a.pot) & 15) == 0;
   if (mm) {  // register-blocked max-plus products (FADD2 + FMNMX3)
-    const size_t s_mm = (size_t)3 * C * C * sizeof(float);
+    const size_t s_mm = ((size_t)C * (C + 4) + (size_t)2 * C * C) * sizeof(float);
     switch (C) {
       case 128:
         if ((e = optin(vch_summary_mm_kernel<128>, g_attr_mm[0], s_mm)) != cudaSuccess) return e;

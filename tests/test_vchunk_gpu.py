@@ -37,8 +37,10 @@ def check(pot_np, lengths_np, dev, Ls):
     E = pot_np.shape[1]
     for L in Ls:
         path, score, flags, kern = run(pot_np, lengths_np, dev, L)
-        if 1 <= L < E and E >= 2 and pot_np.shape[-1] <= 128:  # two staged tiles fit in SMEM
-            assert kern == "vch_summary_kernel", (L, kern)
+        C = pot_np.shape[-1]
+        if 1 <= L < E and E >= 2 and C <= 128:  # two staged tiles fit in SMEM
+            want = "vch_summary_mm_kernel" if C in (32, 64, 128) else "vch_summary_kernel"
+            assert kern == want, (L, kern)
         np.testing.assert_array_equal(flags, f_ref, err_msg=f"L={L}")
         np.testing.assert_array_equal(path, p_ref, err_msg=f"L={L}")
         ok = f_ref == 0
@@ -84,3 +86,41 @@ def test_max_semiring_logz_and_indicator(dev):
     m1, l1, g1 = tsb.marginals(pot, semiring="max")
     assert torch.equal(lz0, lz1) and torch.equal(f0, f1)
     assert torch.equal(m0, m1) and torch.equal(l0, l1) and torch.equal(g0, g1)
+
+
+@pytest.mark.parametrize("C", [32, 64, 128])
+def test_mm_summaries_equal_row_chains(dev, C):
+    """The register-blocked max-plus summaries (FADD2 + 3-input max over strided 8x8 blocks)
+    and the row-chain summaries give the identical path and score (and both the oracle's),
+    with ragged lengths, a -inf sequence and NaN potentials."""
+    B, N = 3, 150
+    pot = tsgen.potentials(B, N, C, seed=77 + C, s=tsgen.quantum(N - 1))
+    lengths = np.array([150, 97, 150], dtype=np.int32)
+    pot[2, 40, 3, 5] = np.nan
+    try:
+        for mm in (True, False):
+            tsb.set_vchunk_mm(mm)
+            if mm:
+                check(pot, lengths, dev, [1, 13, 64])
+            out = run(pot, lengths, dev, 13)
+            assert out[3] == ("vch_summary_mm_kernel" if mm else "vch_summary_kernel")
+            if mm:
+                ref = out
+            else:
+                for a, b in zip(ref[:3], out[:3]):
+                    np.testing.assert_array_equal(a, b)
+    finally:
+        tsb.set_vchunk_mm(True)
+
+
+@pytest.mark.parametrize("B,N,C", [(1, 4097, 64), (2, 2049, 128), (6, 1500, 32)])
+def test_auto_plan_chunks_long_chains(dev, B, N, C):
+    """With the knob at auto (0), few long chains with C in {32, 64, 128} take the chunked
+    scan (abi.cu vit_chunk's calibrated rule) and stay bit-identical to the oracle."""
+    pot = tsgen.potentials(B, N, C, seed=31 + N, s=tsgen.quantum(N - 1))
+    p_ref, s_ref, f_ref = oracle.chain_viterbi(pot, None, threads=8)
+    path, score, flags, kern = run(pot, None, dev, 0)
+    assert kern == "vch_summary_mm_kernel", kern
+    np.testing.assert_array_equal(flags, f_ref)
+    np.testing.assert_array_equal(path, p_ref)
+    assert (score == s_ref.astype(np.float32)).all()
