@@ -364,6 +364,11 @@ TS_API void ts_set_meet(int enable);
  * automatic plan then keeps the serial sweep).  Results are bit-identical. */
 TS_API void ts_set_vchunk_mm(int enable);
 
+/* Debug/testing knob (process-global) for ts_kbest: lanes per label column S in {1, 2, 4, 8}
+ * (0 = automatic: 2 when B >= #SMs, else 8; capped so that C * S <= 512).  Results are
+ * bit-identical for every S. */
+TS_API void ts_set_kbest_split(int S);
+
 /* Debug/testing knob (process-global) for the Viterbi forward with C in {128, 256}:
  * 0 (default) = automatic cluster column split (the largest G in {1,2,4,8} with B*G CTAs
  * fitting the SMs, C/G >= 32); G in {1,2,4,8} = forced cluster size; -1 = the

@@ -495,6 +495,11 @@ def set_vchunk_mm(enable: bool) -> None:
     _lib.load().ts_set_vchunk_mm(1 if enable else 0)
 
 
+def set_kbest_split(S: int) -> None:
+    """Debug knob: K-best lanes per label column (0 auto, 1/2/4/8); results bit-identical."""
+    _lib.load().ts_set_kbest_split(int(S))
+
+
 def set_viterbi_split(G: int) -> None:
     """Debug knob: Viterbi C in {128,256} cluster size (0 auto, 1/2/4/8 forced, -1 legacy)."""
     _lib.load().ts_set_viterbi_split(int(G))

@@ -29,7 +29,7 @@ SYMBOLS = ("ts_workspace_bytes", "ts_logpartition", "ts_marginals", "ts_viterbi"
            "ts_segment_viterbi_maps", "ts_segment_viterbi_finish",
            "ts_kbest_workspace_bytes", "ts_kbest", "ts_semimarkov_workspace_bytes",
            "ts_semimarkov", "ts_semimarkov_viterbi_workspace_bytes", "ts_semimarkov_viterbi",
-           "ts_set_meet", "ts_set_vchunk_mm", "ts_set_viterbi_split", "ts_set_host_graphs",
+           "ts_set_meet", "ts_set_vchunk_mm", "ts_set_kbest_split", "ts_set_viterbi_split", "ts_set_host_graphs",
            "ts_host_alloc", "ts_host_free", "ts_set_tc_summary", "ts_get_tc_summary",
            "ts_last_launch_count", "ts_last_kernel", "ts_status_str", "ts_version")
 
@@ -110,6 +110,8 @@ def load():
     L.ts_set_meet.restype = None
     L.ts_set_vchunk_mm.argtypes = [INT]
     L.ts_set_vchunk_mm.restype = None
+    L.ts_set_kbest_split.argtypes = [INT]
+    L.ts_set_kbest_split.restype = None
     L.ts_set_viterbi_split.argtypes = [INT]
     L.ts_set_viterbi_split.restype = None
     L.ts_set_host_graphs.argtypes = [INT]

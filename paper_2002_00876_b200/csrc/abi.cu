@@ -1694,6 +1694,7 @@ TS_API ts_status ts_segment_finish(const ts_chain* local, int64_t edge_begin, in
 
 TS_API void ts_set_meet(int enable) { g_meet.store(enable ? 1 : 0); }
 TS_API void ts_set_vchunk_mm(int enable) { set_vchunk_mm(enable); }
+TS_API void ts_set_kbest_split(int S) { set_kbest_split(S); }
 TS_API void ts_set_viterbi_split(int G) {
   g_vsplit.store((G == -1 || G == 1 || G == 2 || G == 4 || G == 8) ? G : 0);
 }

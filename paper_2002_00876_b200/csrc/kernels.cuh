@@ -245,7 +245,8 @@ struct KbestArgs {
   uint32_t* flags;   // [B] or nullptr
 };
 int kbest_km(int64_t K);
-size_t kbest_smem(int64_t C, int64_t K);
+size_t kbest_smem(int64_t C, int64_t K, int S);
+void set_kbest_split(int S);  // debug: lanes per column (0 auto, 1/2/4/8)
 cudaError_t launch_kbest(const KbestArgs& a, cudaStream_t st);
 
 // ---- time-sharded Viterbi segments (vseg.cu) -------------------------------

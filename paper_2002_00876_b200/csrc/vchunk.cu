@@ -426,8 +426,10 @@ size_t vch_smem(int C, int extra_floats) {
 }
 template <typename K>
 cudaError_t optin(K kern, std::atomic<uint64_t>& mask, size_t smem) {
+  // the attribute is set once per kernel and device, so to the bound of every size a launch
+  // may ask for (vchunk_ok: <= 200 KB), not to this call's size
   if (smem <= 48 * 1024) return cudaSuccess;
-  return smem_optin_once(kern, mask, (int)smem);
+  return smem_optin_once(kern, mask, 200 * 1024);
 }
 std::atomic<uint64_t> g_attr_sum{0}, g_attr_fwd{0}, g_attr_mm[3];
 std::atomic<int> g_vch_mm{1};

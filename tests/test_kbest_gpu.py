@@ -18,6 +18,14 @@ def _coarse(B, N, C, seed):
             ).astype(np.float32)
 
 
+@pytest.fixture(autouse=True, params=[0, 1, 2, 8])
+def _split(request):
+    """Every case under the automatic lanes-per-column choice and forced S = 1, 2, 8."""
+    tsb.set_kbest_split(request.param)
+    yield
+    tsb.set_kbest_split(0)
+
+
 def _check(pot, K, dev, lengths=None):
     p_ref, s_ref, f_ref = oracle.chain_kbest(pot, K, lengths)
     lt = torch.from_numpy(lengths).to(dev) if lengths is not None else None
@@ -55,3 +63,18 @@ def test_kbest_lengths_flags_short(dev):
     pot[3, 2, 1, 1] = np.nan               # NONFINITE
     lengths = np.array([7, 1, 7, 7, 0, 2], np.int32)   # len 1, BADLEN, len 2 (9 labelings)
     _check(pot, 12, dev, lengths)
+
+
+@pytest.mark.parametrize("C,K", [(20, 8), (64, 4), (128, 16), (5, 16)])
+def test_kbest_sparse_support(dev, C, K):
+    """Most transitions -inf (a banded, partly masked support): columns often have fewer than
+    KM finite heads, so the step's pruning bound T (the KM-th largest head) is -inf and only
+    the finite candidates may enter; plus coarse ties on the finite entries."""
+    B, N = 3, 33
+    rng = np.random.default_rng(C * 7 + K)
+    pot = (rng.integers(-2, 3, size=(B, N - 1, C, C)) * 0.5).astype(np.float32)
+    i, j = np.meshgrid(np.arange(C), np.arange(C), indexing="ij")
+    band = np.abs(i - j) <= 1
+    pot[:, :, ~band] = -np.inf
+    pot[rng.random(pot.shape) < 0.3] = -np.inf
+    _check(pot, K, dev)
