@@ -490,8 +490,16 @@ def run_ours(args):
     hl = tsb.host_empty((B,))
     hf = tsb.host_empty((B,), torch.int32)
     hws = tsb.Workspace(dev)
-    for _ in range(3):
+    # warm-up: at least W calls and >= 60 ms of them — host->device DMA on the GPU boxes ramps
+    # from ~90 to ~26 us per 1.2 MB copy over the first ~30 ms of PCIe traffic in a process
+    # (tools/h2d_warm_probe.py), and the timed region should see the steady state
+    e2e_warm, t_w = 0, time.perf_counter()
+    while e2e_warm < max(3, args.warmup) or time.perf_counter() - t_w < 0.06:
         tsb.marginals_host(hp, hm, hl, hf, device=dev, ws=hws)
+        e2e_warm += 1
+        if e2e_warm % 32 == 0:
+            torch.cuda.synchronize(dev)
+    torch.cuda.synchronize(dev)
     ctx.barrier()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
@@ -545,7 +553,8 @@ def run_ours(args):
                     "h2d_bytes_per_step": B * E * C * C * 4,
                     "d2h_bytes_per_step": B * E * C * C * 4 + 8 * B,
                     "api": "ts_marginals_host (ts_host_alloc page-locked host buffers; H2D, "
-                           "kernels, D2H inside every call)"},
+                           "kernels, D2H inside every call)",
+                    "steps": e2e_steps, "warmup_calls": e2e_warm},
             "gpu_launches": K * launches_per_step,
             "clocks": sampler.summary(),
             "side": side,
