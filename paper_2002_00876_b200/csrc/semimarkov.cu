@@ -14,6 +14,8 @@
 //   mu[n,k-1,c1,c2] = exp(alpha_n[c1] + l[n,k-1,c1,c2] + beta_{n+k}[c2] - A)
 // (0 for parts beyond the sequence).  Flags as the linear chain.  With K = 1 this is also
 // the exact fallback of ts_logpartition / ts_marginals for long chains with 128 < C <= 256.
+#include <atomic>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -439,12 +441,10 @@ cudaError_t launch_semimarkov_viterbi(const SemiVitArgs& a0, cudaStream_t st) {
   a.staged = (size_t)2 * a.K * a.C * a.C * sizeof(float) <= kSemiStageMax ? 1 : 0;
   const int NT = semimarkov_viterbi_threads(a.C);
   const size_t smem = semimarkov_viterbi_smem(a.C, a.K, a.staged != 0);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(semimarkov_viterbi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(semimarkov_viterbi_smem(256, 16, false) + kSemiStageMax));
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0};  // one bit per device (the attribute is per device)
+  const cudaError_t ea = smem_optin_once(semimarkov_viterbi_kernel, attr,
+                                         (int)(semimarkov_viterbi_smem(256, 16, false) + kSemiStageMax));
+  if (ea != cudaSuccess) return ea;
   semimarkov_viterbi_kernel<<<(unsigned)a.B, NT, smem, st>>>(a);
   return cudaGetLastError();
 }

@@ -21,7 +21,13 @@ int main(int argc, char** argv) {
   a.pot = pot; a.lengths = nullptr; a.B = NCTA; a.N = N; a.C = C; a.L = L; a.P = 1; a.Ppad = 1;
   a.nodes = 1; a.H = 0; a.mat = mat; a.off = off; a.ident = ident; a.cflag = cflag; a.wflags = wflags;
   if (getenv("TC1")) set_tc_summary(1);
-  for (int it = 0; it < 3; ++it) launch_summary_tc(a, 0);
+  {
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, summary_tc_kernel<3, 128>);
+    printf("summary_tc<3,128>: regs %d, maxThreadsPerBlock %d, local %zu B, static smem %zu\n", fa.numRegs,
+           fa.maxThreadsPerBlock, fa.localSizeBytes, fa.sharedSizeBytes);
+  }
+  for (int it = 0; it < 3; ++it) { cudaError_t le = launch_summary_tc(a, 0); if (le != cudaSuccess) printf("launch: %s\n", cudaGetErrorString(le)); }
   cudaDeviceSynchronize();
   static long long t[64][8];
 #ifdef TS_TC_TIMING
