@@ -1,5 +1,6 @@
-"""cfg5 (B=4, N=65536, C=128) Viterbi on one GPU: the serial sweeps (vit2 cluster split, one CTA)
-and the time-chunked max-plus scan (vchunk.cu) at a few chunk lengths.  CUDA events, one
+"""cfg5 (B=4, N=65536, C=128) Viterbi on one GPU: the serial sweeps (vit2 cluster split, one CTA;
+plan chunk >= N forces the serial plan), the default auto plan, and the time-chunked max-plus
+scan (vchunk.cu) at a few chunk lengths.  CUDA events, one
 timed call after a warm-up call per variant."""
 import sys, os, json, torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -13,8 +14,8 @@ def t(fn):
     e0.record(); fn(); e1.record(); torch.cuda.synchronize()
     return e0.elapsed_time(e1)
 ref = None
-for name, vs, L in [("serial vit2", 0, 0), ("serial one-CTA", -1, 0), ("chunked L=512", 0, 512),
-                    ("chunked L=1772", 0, 1772), ("chunked L=4096", 0, 4096)]:
+for name, vs, L in [("serial vit2", 0, cfg.N), ("auto plan", 0, 0), ("serial one-CTA", -1, cfg.N),
+                    ("chunked L=512", 0, 512), ("chunked L=1772", 0, 1772), ("chunked L=4096", 0, 4096)]:
     tsb.set_viterbi_split(vs); tsb.set_plan_chunk(L)
     ms = t(lambda: tsb.viterbi(pot))
     path, score, flags = tsb.viterbi(pot)
