@@ -351,6 +351,13 @@ TS_API void ts_set_tiny(int enable);
  * parity tolerances. */
 TS_API void ts_set_wide_ring(int enable);
 
+/* Debug/testing knob (process-global): 1 (default) lets the short-chain kernel fb_tiny read
+ * its inputs before waiting for a still-running earlier call on the stream (programmatic
+ * dependent launch), so consecutive calls overlap everything but their global writes — when
+ * the library has not recorded a recent call whose outputs overlap this call's pot / lengths
+ * (then it waits before reading, as with 0).  Results are identical either way. */
+TS_API void ts_set_tiny_early(int enable);
+
 /* Debug/testing knob (process-global): 1 (default) runs ts_marginals for C = 64 with one
  * serial chunk per sequence as the meet-in-the-middle kernel (forward and backward
  * recursions concurrently from both ends, marginals fused); 0 = separate forward and

@@ -484,6 +484,12 @@ def set_wide_ring(enable: bool) -> None:
     _lib.load().ts_set_wide_ring(1 if enable else 0)
 
 
+def set_tiny_early(enable: bool) -> None:
+    """Debug knob: fb_tiny reads its inputs before the PDL wait when no recent call's outputs
+    overlap them (default on); off = wait first.  Identical results."""
+    _lib.load().ts_set_tiny_early(1 if enable else 0)
+
+
 def set_meet(enable: bool) -> None:
     """Debug knob: meet-in-the-middle fused marginals kernel for C = 64 (default on)."""
     _lib.load().ts_set_meet(1 if enable else 0)

@@ -24,7 +24,7 @@ STATUS = {0: "TS_OK", 1: "TS_E_INVALID", 2: "TS_E_UNSUPPORTED", 3: "TS_E_WORKSPA
 SYMBOLS = ("ts_workspace_bytes", "ts_logpartition", "ts_marginals", "ts_viterbi",
            "ts_marginals_host", "ts_segment_summary_bytes", "ts_segment_summary",
            "ts_segment_finish", "ts_set_plan_chunk", "ts_get_plan_chunk", "ts_set_small_cluster",
-           "ts_set_tiny", "ts_set_wide_ring", "ts_set_host_pipeline", "ts_entropy", "ts_expectation", "ts_log_prob", "ts_sample",
+           "ts_set_tiny", "ts_set_wide_ring", "ts_set_tiny_early", "ts_set_host_pipeline", "ts_entropy", "ts_expectation", "ts_log_prob", "ts_sample",
            "ts_segment_viterbi_summary_bytes", "ts_segment_viterbi_summary",
            "ts_segment_viterbi_maps", "ts_segment_viterbi_finish",
            "ts_kbest_workspace_bytes", "ts_kbest", "ts_semimarkov_workspace_bytes",
@@ -104,6 +104,8 @@ def load():
     L.ts_set_tiny.restype = None
     L.ts_set_wide_ring.argtypes = [INT]
     L.ts_set_wide_ring.restype = None
+    L.ts_set_tiny_early.argtypes = [INT]
+    L.ts_set_tiny_early.restype = None
     L.ts_set_host_pipeline.argtypes = [INT]
     L.ts_set_host_pipeline.restype = None
     L.ts_set_meet.argtypes = [INT]

@@ -648,7 +648,8 @@ struct HostKey {
 int64_t knob_word() {
   return (int64_t)g_meet.load() | ((int64_t)g_small_cluster.load() << 1) |
          ((int64_t)tsb::get_tc_summary() << 4) | ((int64_t)g_tiny.load() << 8) |
-         ((int64_t)(g_vsplit.load() + 1) << 9) | ((int64_t)(tsb::g_wide_ring != 0) << 14);
+         ((int64_t)(g_vsplit.load() + 1) << 9) | ((int64_t)(tsb::g_wide_ring != 0) << 14) |
+         ((int64_t)tsb::get_tiny_early() << 15);
 }
 
 struct HostGraph {
@@ -1705,6 +1706,7 @@ TS_API void ts_set_small_cluster(int G) {
 }
 TS_API void ts_set_tiny(int enable) { g_tiny.store(enable ? 1 : 0); }
 TS_API void ts_set_wide_ring(int enable) { g_wide_ring = enable ? 1 : 0; }
+TS_API void ts_set_tiny_early(int enable) { tsb::set_tiny_early(enable); }
 TS_API int ts_last_launch_count(void) { return t_launches; }
 TS_API const char* ts_last_kernel(void) { return t_kernel; }
 

@@ -1,5 +1,7 @@
 // fb_tiny.cu — the fb_tiny kernel (one CTA per sequence) and its launcher; the
 // device code lives in tiny.cuh (shared with the cluster scan's exact fallback).
+#include <mutex>
+
 #include "tiny.cuh"
 
 namespace tsb {
@@ -20,6 +22,57 @@ bool tiny_fits(const SmallArgs& a) {
   if ((reinterpret_cast<uintptr_t>(a.pot) & 15) != 0) return false;
   if (a.marg && (reinterpret_cast<uintptr_t>(a.marg) & 15) != 0) return false;
   return tiny_smem_bytes(a.N, C) <= (size_t)200 * 1024;
+}
+
+// ---- early input reads (SmallArgs::early) --------------------------------------------------
+// fb_tiny and fb_cscan trigger their dependents (griddepcontrol.launch_dependents) as they
+// start, so a call may begin while earlier calls on the stream still run.  A call may read its
+// inputs before its PDL wait only if none of those calls writes them: the outputs of the most
+// recent PDL launches (more than the device can hold resident at once) are kept here and a
+// launch whose pot / lengths ranges meet one of them waits before reading, as before.
+namespace {
+struct ByteRange {
+  uintptr_t lo, hi;
+};
+constexpr int kPdlRing = 512;
+std::mutex g_pdl_mu;
+ByteRange g_pdl_ring[kPdlRing];
+int64_t g_pdl_count = 0;
+std::atomic<int> g_tiny_early{1};
+
+ByteRange range_of(const void* p, int64_t bytes) {
+  const uintptr_t lo = reinterpret_cast<uintptr_t>(p);
+  return ByteRange{lo, lo + (uintptr_t)(bytes > 0 ? bytes : 0)};
+}
+bool ring_hit(const ByteRange& r) {
+  if (r.hi <= r.lo) return false;
+  const int64_t n = g_pdl_count < kPdlRing ? g_pdl_count : kPdlRing;
+  for (int64_t i = 0; i < n; ++i)
+    if (r.lo < g_pdl_ring[i].hi && g_pdl_ring[i].lo < r.hi) return true;
+  return false;
+}
+void ring_add(const ByteRange& r) {
+  if (r.hi <= r.lo) return;
+  g_pdl_ring[g_pdl_count % kPdlRing] = r;
+  ++g_pdl_count;
+}
+}  // namespace
+
+void set_tiny_early(int on) { g_tiny_early.store(on ? 1 : 0); }
+int get_tiny_early() { return g_tiny_early.load(); }
+
+// Records the outputs of a PDL-triggering launch; returns whether its inputs are clear of
+// every recorded output (checked before this launch's own outputs are added).
+bool pdl_launch_note(const SmallArgs& a) {
+  const int64_t E = a.N - 1 > 0 ? a.N - 1 : 0, nel = a.B * E * a.C * a.C;
+  std::lock_guard<std::mutex> lock(g_pdl_mu);
+  const bool clear = !ring_hit(range_of(a.pot, nel * 4)) &&
+                     !(a.lengths && ring_hit(range_of(a.lengths, a.B * 4)));
+  if (a.marg) ring_add(range_of(a.marg, nel * 4));
+  ring_add(range_of(a.logz, a.B * 4));
+  if (a.flags) ring_add(range_of(a.flags, a.B * 4));
+  if (a.xmode && a.xout) ring_add(range_of(a.xout, a.B * 4));
+  return clear;
 }
 
 namespace {
@@ -49,7 +102,10 @@ cudaError_t launch_tiny_c(const SmallArgs& a, size_t smem, cudaStream_t st) {
 }
 }  // namespace
 
-cudaError_t launch_tiny(const SmallArgs& a, cudaStream_t st) {
+cudaError_t launch_tiny(const SmallArgs& a0, cudaStream_t st) {
+  SmallArgs a = a0;
+  const bool clear = pdl_launch_note(a);
+  a.early = (clear && g_tiny_early.load()) ? 1 : 0;
   const size_t smem = tiny_smem_bytes(a.N, a.C);
   switch (a.C) {
     case 4: return launch_tiny_c<4>(a, smem, st);

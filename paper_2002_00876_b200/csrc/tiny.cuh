@@ -626,8 +626,9 @@ __device__ __forceinline__ void tiny_marginals(const float* __restrict__ EXB, co
 
 // The whole-sequence body: one CTA of kTinyThreads threads processes sequence b with the
 // shared memory at `sm` (tiny_layout).  PROLOGUE: this call owns the PDL handshake
-// (launch_dependents, L2 prefetch, griddepcontrol.wait); the cluster scan's exact fallback
-// calls it with PROLOGUE = false after its own prologue.
+// (launch_dependents, L2 prefetch, griddepcontrol.wait — before the first read, or with
+// a.early before each thread's first global write); the cluster scan's exact fallback calls
+// it with PROLOGUE = false after its own prologue.
 template <int C, bool PROLOGUE, int XM = 0>
 __device__ __forceinline__ void tiny_body(const SmallArgs& a, const int64_t b, float* __restrict__ sm) {
   constexpr int CC = C * C, Q4 = CC / 4;
@@ -668,13 +669,14 @@ __device__ __forceinline__ void tiny_body(const SmallArgs& a, const int64_t b, f
                    "r"((uint32_t)(CC * 4))
                    : "memory");
 #endif
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (!a.early) asm volatile("griddepcontrol.wait;" ::: "memory");
   }
   __syncthreads();
 
   const int64_t len = seq_len(a.lengths, b, N);
   float* mg = a.marg ? a.marg + b * E * CC : nullptr;
   if (len < 0) {  // BADLEN: logZ NaN, marginals 0
+    if (PROLOGUE && a.early) asm volatile("griddepcontrol.wait;" ::: "memory");
     if (mg)
       for (int64_t k = tid; k < E * Q4; k += kTinyThreads)
         reinterpret_cast<float4*>(mg)[k] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -724,6 +726,7 @@ __device__ __forceinline__ void tiny_body(const SmallArgs& a, const int64_t b, f
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
     const float Lf = warp_lse2(lane < C ? node_log(F, HF, Eb, lane) : neg_inf());
+    if (PROLOGUE && a.early) asm volatile("griddepcontrol.wait;" ::: "memory");  // first write
     if (lane == 0) {
       const bool empty = (Lf == neg_inf()) || !(part > -INFINITY);
       a.logz[b] = empty ? neg_inf() : (float)(part + kLn2 * (double)Lf);
@@ -737,6 +740,7 @@ __device__ __forceinline__ void tiny_body(const SmallArgs& a, const int64_t b, f
   } else {
     // ---- marginals: centre edges first, one warp per edge, float4-wide -------------------
     if (mg) {
+      if (PROLOGUE && a.early) asm volatile("griddepcontrol.wait;" ::: "memory");  // first write
       tiny_marginals<C, (C + 1) * tiny_rs(C), XM>(EXB, raw, Tm, F, HF, G, HG, fn, bn, Eb, mg, wi,
                                                   kWorkers, lane, XM == 2 ? a.xr + b * E * CC : nullptr,
                                                   &xacc);
@@ -747,6 +751,7 @@ __device__ __forceinline__ void tiny_body(const SmallArgs& a, const int64_t b, f
   }
   __syncthreads();
   TPHASE(5);
+  if (PROLOGUE && a.early) asm volatile("griddepcontrol.wait;" ::: "memory");  // tail writes
   const unsigned fl = (*sflag & TS_F_NONFINITE) ? (unsigned)TS_F_NONFINITE : *sflag;
   if (tid == 0 && a.flags) a.flags[b] = fl;
   if ((fl & TS_F_NONFINITE) && tid == 0) a.logz[b] = qnan();

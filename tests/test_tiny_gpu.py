@@ -144,3 +144,44 @@ def test_mixed_fast_and_fallback_sequences(dev, C):
     lengths[5] = 4
     lengths[6] = 2 * 4 + 1
     parity(pot.astype(np.float32), lengths, dev)
+
+
+def _chain_run(pot, steps, early, lengths=None):
+    """x_{i+1} = marginals(x_i) back to back on one stream (each call reads the buffer the
+    previous call is writing), plus independent calls on rotating buffers; no host sync."""
+    tsb.set_tiny_early(early)
+    try:
+        xs = [pot]
+        lzs = []
+        for _ in range(steps):
+            m, lz, fl = tsb.marginals(xs[-1], lengths)
+            xs.append(m)
+            lzs.append(lz)
+        indep = [tsb.marginals(pot + float(k), lengths)[1] for k in range(8)]
+        torch.cuda.synchronize()
+        return xs, lzs, indep
+    finally:
+        tsb.set_tiny_early(True)
+
+
+@pytest.mark.parametrize("C", [8, 20])
+def test_tiny_early_reads_chained_calls(dev, C, plan):
+    """Consecutive calls overlap (PDL) and read their inputs before waiting for the previous
+    call when no recent call's outputs overlap them: a call whose potentials are the previous
+    call's marginals must still see them complete — identical to waiting first, and the
+    first link checked against the oracle."""
+    B, N = 6, 25
+    pot_np = tsgen.potentials(B, N, C, seed=41 + C)
+    lengths_np = np.array([N, N - 3, 1, N, 7, N], np.int32)
+    pot = torch.from_numpy(pot_np).to(dev)
+    lengths = torch.from_numpy(lengths_np).to(dev)
+    xs1, lz1, ind1 = _chain_run(pot, 12, True, lengths)
+    xs0, lz0, ind0 = _chain_run(pot, 12, False, lengths)
+    for a, b in zip(xs1, xs0):
+        assert torch.equal(a, b)
+    for a, b in zip(lz1 + ind1, lz0 + ind0):
+        assert torch.equal(torch.nan_to_num(a, nan=7.0), torch.nan_to_num(b, nan=7.0))
+    x1 = xs1[1].cpu().numpy()
+    lz_ref, mg_ref, _ = oracle.chain_marginals(x1, lengths_np, threads=8)
+    check_logz(lz1[1].cpu().numpy(), lz_ref)
+    check_marg(xs1[2].cpu().numpy(), mg_ref)
