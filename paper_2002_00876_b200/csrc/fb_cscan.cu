@@ -458,7 +458,7 @@ cudaError_t launch_cs_g(const SmallArgs& a, size_t smem, cudaStream_t st) {
 }  // namespace
 
 cudaError_t launch_cscan(const SmallArgs& a, int G, cudaStream_t st) {
-  (void)pdl_launch_note(a);  // it triggers its dependents early: its outputs are recorded
+  (void)pdl_launch_note(a);  // it triggers its dependents early: its ranges are recorded
   const size_t smem = cscan_smem_bytes(a.N, a.C, G);
   if (G == 4) return launch_cs_g<4>(a, smem, st);
   if (G == 2) return launch_cs_g<2>(a, smem, st);

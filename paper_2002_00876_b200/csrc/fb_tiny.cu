@@ -24,55 +24,78 @@ bool tiny_fits(const SmallArgs& a) {
   return tiny_smem_bytes(a.N, C) <= (size_t)200 * 1024;
 }
 
-// ---- early input reads (SmallArgs::early) --------------------------------------------------
+// ---- early input reads / early marginal writes (SmallArgs::early) --------------------------
 // fb_tiny and fb_cscan trigger their dependents (griddepcontrol.launch_dependents) as they
-// start, so a call may begin while earlier calls on the stream still run.  A call may read its
-// inputs before its PDL wait only if none of those calls writes them: the outputs of the most
-// recent PDL launches (more than the device can hold resident at once) are kept here and a
-// launch whose pot / lengths ranges meet one of them waits before reading, as before.
+// start, so a call may begin while earlier calls on the stream still run — at most the last
+// kPdlWindow such launches (a device holds at most 128 resident grids, and a grid triggers only
+// once all of its CTAs are resident).  The input and output ranges of recent launches are kept
+// here: a launch may read its inputs before its PDL wait if no launch in the window writes
+// them, and may also write its marginals before the wait if no launch in the window reads or
+// writes that range (every thread still waits before the per-sequence scalars and before it
+// exits, so a call completes only after its predecessor).
 namespace {
-struct ByteRange {
+struct PdlRange {
   uintptr_t lo, hi;
+  int64_t seq;
+  bool out;
 };
-constexpr int kPdlRing = 512;
+constexpr int kPdlRing = 2048;
+constexpr int64_t kPdlWindow = 130;
 std::mutex g_pdl_mu;
-ByteRange g_pdl_ring[kPdlRing];
-int64_t g_pdl_count = 0;
+PdlRange g_pdl_ring[kPdlRing];
+int64_t g_pdl_n = 0;    // ranges recorded
+int64_t g_pdl_seq = 0;  // launches recorded
 std::atomic<int> g_tiny_early{1};
 
-ByteRange range_of(const void* p, int64_t bytes) {
+PdlRange range_of(const void* p, int64_t bytes, bool out) {
   const uintptr_t lo = reinterpret_cast<uintptr_t>(p);
-  return ByteRange{lo, lo + (uintptr_t)(bytes > 0 ? bytes : 0)};
+  return PdlRange{lo, p ? lo + (uintptr_t)(bytes > 0 ? bytes : 0) : lo, g_pdl_seq, out};
 }
-bool ring_hit(const ByteRange& r) {
+// any range of a launch in the window overlapping r (outputs only, or inputs and outputs)?
+bool window_hit(const PdlRange& r, bool outputs_only) {
   if (r.hi <= r.lo) return false;
-  const int64_t n = g_pdl_count < kPdlRing ? g_pdl_count : kPdlRing;
-  for (int64_t i = 0; i < n; ++i)
-    if (r.lo < g_pdl_ring[i].hi && g_pdl_ring[i].lo < r.hi) return true;
+  const int64_t n = g_pdl_n < kPdlRing ? g_pdl_n : kPdlRing;
+  for (int64_t i = 0; i < n; ++i) {
+    const PdlRange& q = g_pdl_ring[i];
+    if (q.seq <= g_pdl_seq - kPdlWindow || (outputs_only && !q.out)) continue;
+    if (r.lo < q.hi && q.lo < r.hi) return true;
+  }
   return false;
 }
-void ring_add(const ByteRange& r) {
+void ring_add(const PdlRange& r) {
   if (r.hi <= r.lo) return;
-  g_pdl_ring[g_pdl_count % kPdlRing] = r;
-  ++g_pdl_count;
+  g_pdl_ring[g_pdl_n % kPdlRing] = r;
+  ++g_pdl_n;
 }
 }  // namespace
 
 void set_tiny_early(int on) { g_tiny_early.store(on ? 1 : 0); }
 int get_tiny_early() { return g_tiny_early.load(); }
 
-// Records the outputs of a PDL-triggering launch; returns whether its inputs are clear of
-// every recorded output (checked before this launch's own outputs are added).
-bool pdl_launch_note(const SmallArgs& a) {
+// Records the inputs and outputs of a dependents-triggering launch; returns SmallArgs::early
+// for it (0: wait first; 1: read early; 3: read early and write the marginals early), checked
+// against the launches before it.  (A ring this size never drops an entry of the window.)
+int pdl_launch_note(const SmallArgs& a) {
   const int64_t E = a.N - 1 > 0 ? a.N - 1 : 0, nel = a.B * E * a.C * a.C;
   std::lock_guard<std::mutex> lock(g_pdl_mu);
-  const bool clear = !ring_hit(range_of(a.pot, nel * 4)) &&
-                     !(a.lengths && ring_hit(range_of(a.lengths, a.B * 4)));
-  if (a.marg) ring_add(range_of(a.marg, nel * 4));
-  ring_add(range_of(a.logz, a.B * 4));
-  if (a.flags) ring_add(range_of(a.flags, a.B * 4));
-  if (a.xmode && a.xout) ring_add(range_of(a.xout, a.B * 4));
-  return clear;
+  const PdlRange in_pot = range_of(a.pot, nel * 4, false);
+  const PdlRange in_len = range_of(a.lengths, a.B * 4, false);
+  const PdlRange in_xr = range_of(a.xmode == 2 ? a.xr : nullptr, nel * 4, false);
+  const PdlRange out_m = range_of(a.marg, nel * 4, true);
+  int early = 0;
+  if (!window_hit(in_pot, true) && !window_hit(in_len, true) && !window_hit(in_xr, true)) {
+    early = 1;
+    if (a.marg && !window_hit(out_m, false)) early = 3;
+  }
+  ring_add(in_pot);
+  ring_add(in_len);
+  ring_add(in_xr);
+  ring_add(out_m);
+  ring_add(range_of(a.logz, a.B * 4, true));
+  ring_add(range_of(a.flags, a.B * 4, true));
+  ring_add(range_of(a.xmode ? a.xout : nullptr, a.B * 4, true));
+  ++g_pdl_seq;
+  return early;
 }
 
 namespace {
@@ -104,8 +127,8 @@ cudaError_t launch_tiny_c(const SmallArgs& a, size_t smem, cudaStream_t st) {
 
 cudaError_t launch_tiny(const SmallArgs& a0, cudaStream_t st) {
   SmallArgs a = a0;
-  const bool clear = pdl_launch_note(a);
-  a.early = (clear && g_tiny_early.load()) ? 1 : 0;
+  const int early = pdl_launch_note(a);
+  a.early = g_tiny_early.load() ? early : 0;
   const size_t smem = tiny_smem_bytes(a.N, a.C);
   switch (a.C) {
     case 4: return launch_tiny_c<4>(a, smem, st);

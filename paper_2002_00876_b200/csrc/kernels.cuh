@@ -25,10 +25,11 @@ struct SmallArgs {
   const float* xr;
   int xmode;
   float* xout;
-  // fb_tiny: 1 = no programmatic (PDL) predecessor that may still run writes pot / lengths
-  // (checked by the launcher against the outputs of its recent PDL launches), so the inputs
-  // are read at once and the wait for the previous grid moves to just before the first
-  // global write: consecutive calls overlap everything but their writes
+  // fb_tiny: bit 0 = no programmatic (PDL) predecessor that may still run writes pot /
+  // lengths / xr (checked by the launcher against its recent PDL launches), so the inputs are
+  // read at once and the wait for the previous grid moves to just before the first global
+  // write; bit 1 = none reads or writes the marginal range either, so the marginals are
+  // written before the wait too (the per-sequence scalars and the exit still wait)
   int early;
 };
 size_t small_smem_bytes(int64_t N, int64_t C);
@@ -38,9 +39,9 @@ cudaError_t launch_small(const SmallArgs& a, cudaStream_t st);
 size_t tiny_smem_bytes(int64_t N, int64_t C);
 bool tiny_fits(const SmallArgs& a);
 cudaError_t launch_tiny(const SmallArgs& a, cudaStream_t st);
-// PDL bookkeeping shared by fb_tiny / fb_cscan launches (fb_tiny.cu): records the outputs
-// of a dependents-triggering launch, returns whether its inputs are clear of the recorded ones
-bool pdl_launch_note(const SmallArgs& a);
+// PDL bookkeeping shared by fb_tiny / fb_cscan launches (fb_tiny.cu): records the inputs and
+// outputs of a dependents-triggering launch, returns its SmallArgs::early value
+int pdl_launch_note(const SmallArgs& a);
 void set_tiny_early(int on);  // fb_tiny early input reads (default 1)
 int get_tiny_early();
 // the chunked scan of §6(a) on a G-CTA cluster per sequence (fb_cscan.cu), same shapes

@@ -740,7 +740,7 @@ __device__ __forceinline__ void tiny_body(const SmallArgs& a, const int64_t b, f
   } else {
     // ---- marginals: centre edges first, one warp per edge, float4-wide -------------------
     if (mg) {
-      if (PROLOGUE && a.early) asm volatile("griddepcontrol.wait;" ::: "memory");  // first write
+      if (PROLOGUE && a.early == 1) asm volatile("griddepcontrol.wait;" ::: "memory");  // first write
       tiny_marginals<C, (C + 1) * tiny_rs(C), XM>(EXB, raw, Tm, F, HF, G, HG, fn, bn, Eb, mg, wi,
                                                   kWorkers, lane, XM == 2 ? a.xr + b * E * CC : nullptr,
                                                   &xacc);
