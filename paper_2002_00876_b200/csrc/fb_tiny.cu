@@ -73,8 +73,8 @@ void set_tiny_early(int on) { g_tiny_early.store(on ? 1 : 0); }
 int get_tiny_early() { return g_tiny_early.load(); }
 
 // Records the inputs and outputs of a dependents-triggering launch; returns SmallArgs::early
-// for it (0: wait first; 1: read early; 3: read early and write the marginals early), checked
-// against the launches before it.  (A ring this size never drops an entry of the window.)
+// for it (0: wait first; bit 0: read early; bit 1: also write the marginals early; bit 2: also
+// write logZ / flags / the fused output early), checked against the launches before it.  (A ring this size never drops an entry of the window.)
 int pdl_launch_note(const SmallArgs& a) {
   const int64_t E = a.N - 1 > 0 ? a.N - 1 : 0, nel = a.B * E * a.C * a.C;
   std::lock_guard<std::mutex> lock(g_pdl_mu);
@@ -82,18 +82,22 @@ int pdl_launch_note(const SmallArgs& a) {
   const PdlRange in_len = range_of(a.lengths, a.B * 4, false);
   const PdlRange in_xr = range_of(a.xmode == 2 ? a.xr : nullptr, nel * 4, false);
   const PdlRange out_m = range_of(a.marg, nel * 4, true);
+  const PdlRange out_l = range_of(a.logz, a.B * 4, true);
+  const PdlRange out_f = range_of(a.flags, a.B * 4, true);
+  const PdlRange out_x = range_of(a.xmode ? a.xout : nullptr, a.B * 4, true);
   int early = 0;
   if (!window_hit(in_pot, true) && !window_hit(in_len, true) && !window_hit(in_xr, true)) {
     early = 1;
-    if (a.marg && !window_hit(out_m, false)) early = 3;
+    if (a.marg && !window_hit(out_m, false)) early |= 2;
+    if (!window_hit(out_l, false) && !window_hit(out_f, false) && !window_hit(out_x, false)) early |= 4;
   }
   ring_add(in_pot);
   ring_add(in_len);
   ring_add(in_xr);
   ring_add(out_m);
-  ring_add(range_of(a.logz, a.B * 4, true));
-  ring_add(range_of(a.flags, a.B * 4, true));
-  ring_add(range_of(a.xmode ? a.xout : nullptr, a.B * 4, true));
+  ring_add(out_l);
+  ring_add(out_f);
+  ring_add(out_x);
   ++g_pdl_seq;
   return early;
 }

@@ -29,7 +29,8 @@ struct SmallArgs {
   // lengths / xr (checked by the launcher against its recent PDL launches), so the inputs are
   // read at once and the wait for the previous grid moves to just before the first global
   // write; bit 1 = none reads or writes the marginal range either, so the marginals are
-  // written before the wait too (the per-sequence scalars and the exit still wait)
+  // written before the wait too; bit 2 = the same for logZ / flags / xout; every thread
+  // still waits before it exits (the call completes after its predecessor)
   int early;
 };
 size_t small_smem_bytes(int64_t N, int64_t C);

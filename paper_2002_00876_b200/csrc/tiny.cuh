@@ -726,7 +726,7 @@ __device__ __forceinline__ void tiny_body(const SmallArgs& a, const int64_t b, f
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
     const float Lf = warp_lse2(lane < C ? node_log(F, HF, Eb, lane) : neg_inf());
-    if (PROLOGUE && a.early) asm volatile("griddepcontrol.wait;" ::: "memory");  // first write
+    if (PROLOGUE && (a.early & 5) == 1) asm volatile("griddepcontrol.wait;" ::: "memory");  // logZ
     if (lane == 0) {
       const bool empty = (Lf == neg_inf()) || !(part > -INFINITY);
       a.logz[b] = empty ? neg_inf() : (float)(part + kLn2 * (double)Lf);
@@ -740,7 +740,7 @@ __device__ __forceinline__ void tiny_body(const SmallArgs& a, const int64_t b, f
   } else {
     // ---- marginals: centre edges first, one warp per edge, float4-wide -------------------
     if (mg) {
-      if (PROLOGUE && a.early == 1) asm volatile("griddepcontrol.wait;" ::: "memory");  // first write
+      if (PROLOGUE && (a.early & 3) == 1) asm volatile("griddepcontrol.wait;" ::: "memory");  // marginals
       tiny_marginals<C, (C + 1) * tiny_rs(C), XM>(EXB, raw, Tm, F, HF, G, HG, fn, bn, Eb, mg, wi,
                                                   kWorkers, lane, XM == 2 ? a.xr + b * E * CC : nullptr,
                                                   &xacc);
@@ -751,7 +751,7 @@ __device__ __forceinline__ void tiny_body(const SmallArgs& a, const int64_t b, f
   }
   __syncthreads();
   TPHASE(5);
-  if (PROLOGUE && a.early) asm volatile("griddepcontrol.wait;" ::: "memory");  // tail writes
+  if (PROLOGUE && (a.early & 5) == 1) asm volatile("griddepcontrol.wait;" ::: "memory");  // tail writes
   const unsigned fl = (*sflag & TS_F_NONFINITE) ? (unsigned)TS_F_NONFINITE : *sflag;
   if (tid == 0 && a.flags) a.flags[b] = fl;
   if ((fl & TS_F_NONFINITE) && tid == 0) a.logz[b] = qnan();
@@ -773,6 +773,9 @@ __device__ __forceinline__ void tiny_body(const SmallArgs& a, const int64_t b, f
       a.xout[b] = bad ? qnan() : (float)(XM == 1 ? (double)lz - tot : tot);
     }
   }
+  // every thread waits before it exits: the call completes only after its predecessor, so
+  // everything after it on the stream stays ordered after both
+  if (PROLOGUE && a.early) asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 // The cluster scan's exact fallback: one non-inlined copy of the body, so the cluster

@@ -185,3 +185,25 @@ def test_tiny_early_reads_chained_calls(dev, C, plan):
     lz_ref, mg_ref, _ = oracle.chain_marginals(x1, lengths_np, threads=8)
     check_logz(lz1[1].cpu().numpy(), lz_ref)
     check_marg(xs1[2].cpu().numpy(), mg_ref)
+
+
+def test_tiny_early_war_hazard(dev, plan):
+    """A call whose marginal buffer is the potentials of a call that may still be running
+    (write-after-read) must not write them before that call has read them; nor may it write
+    the logZ buffer an earlier call is writing (write-after-write)."""
+    B, N, C = 32, 25, 20
+    x_np = tsgen.potentials(B, N, C, seed=77)
+    y_np = tsgen.potentials(B, N, C, seed=78)
+    lz_x, mg_x, _ = oracle.chain_marginals(x_np, threads=8)
+    lz_y, mg_y, _ = oracle.chain_marginals(y_np, threads=8)
+    for _ in range(3):
+        x = torch.from_numpy(x_np).to(dev)
+        y = torch.from_numpy(y_np).to(dev)
+        torch.cuda.synchronize()
+        m1, l1, f1 = tsb.marginals(x)           # reads x
+        m2, l2, f2 = tsb.marginals(y, out=x)    # overwrites x with y's marginals
+        torch.cuda.synchronize()
+        check_logz(l1.cpu().numpy(), lz_x)
+        check_marg(m1.cpu().numpy(), mg_x)
+        check_logz(l2.cpu().numpy(), lz_y)
+        check_marg(m2.cpu().numpy(), mg_y)
