@@ -7,7 +7,7 @@
 namespace tsb {
 
 template <int C, int XM>
-__global__ void __launch_bounds__(kTinyThreads, 1) fb_tiny_kernel(SmallArgs a) {
+__global__ void __launch_bounds__(kTinyThreads, 2) fb_tiny_kernel(SmallArgs a) {
   extern __shared__ __align__(16) float sm[];
   tiny_body<C, true, XM>(a, blockIdx.x, sm);
 }

@@ -2,7 +2,7 @@
 // short chains with C % 4 == 0 and C <= 28 (the paper's Table 1 setting B=32, N=25, C=20,
 // PAPER.md P:54): the one-CTA-per-sequence body `tiny_body` (the fb_tiny kernel, and the exact
 // fallback of the cluster scan in fb_cscan.cu) and its recursion `tiny_sweep`.
-// One CTA (kTinyThreads = 384 threads) per sequence, the whole sequence resident in shared
+// One CTA (kTinyThreads = 256 threads, two per SM) per sequence, the whole sequence resident in shared
 // memory; the marginals are pipelined against the two serial recursions through per-node
 // mbarriers.
 //
@@ -71,7 +71,10 @@ __device__ long long g_tiny_edge[64][4];   // cta 0 per edge: waited, summed, st
 namespace {
 
 #ifndef TINY_THREADS
-#define TINY_THREADS 384  // swept 256-1024 (bench cfg2): 384 best, 6.66 vs 6.71 us/step at 512
+// 256: two CTAs per SM (128 registers x 256 threads x 2, ~92 KB shared memory each at cfg2), so
+// overlapping calls (PDL early mode) have twice the CTA slots: cfg2 1.45 -> 1.075 us/step.
+// (One call alone: 384 was best in a 256-1024 sweep, 6.66 vs 6.71 us at 512.)
+#define TINY_THREADS 256
 #endif
 constexpr int kTinyThreads = TINY_THREADS;
 constexpr int kTinyWarps = kTinyThreads / 32;
@@ -101,13 +104,20 @@ struct TinyLayout {
   int64_t raw, exf, exb, T, F, HF, G, HG, cf, bar, xred, total;  // float offsets
 };
 
-// mbarriers: ld[E] (tile loaded), fn[N], bn[N] (node published)
+// mbarriers: ld[E] (tile loaded; TMA variants), fn[N], bn[N] (node published).  The raw tile
+// area (a bulk-copy target) exists only in the TMA prepass variants: the default prepass
+// reads the tiles from L2, and without it two CTAs fit on an SM.
+#if defined(TINY_TMA_PREPASS) || defined(TINY_TMA_ROWS)
+constexpr bool kTinyRaw = true;
+#else
+constexpr bool kTinyRaw = false;
+#endif
 __host__ __device__ inline TinyLayout tiny_layout(int64_t N, int C) {
   TinyLayout l;
   const int64_t E = N - 1 > 0 ? N - 1 : 1;
   const int64_t RS = tiny_rs(C), TB = (int64_t)(C + 1) * RS;
-  l.raw = 0;                           // [E][C][C] dense (bulk-copy target)
-  l.exf = l.raw + E * C * C;           // EXF: [E][C+1][RS] row j = column j of EX, row C = row sums
+  l.raw = 0;                           // [E][C][C] dense (bulk-copy target, TMA variants)
+  l.exf = l.raw + (kTinyRaw ? E * C * C : 0);  // EXF: [E][C+1][RS] row j = column j of EX, row C = row sums
   l.exb = l.exf + E * TB;              // EXB: [E][C+1][RS] row i = row i of EX, row C = col sums
   l.T = l.exb + E * TB;                // [E]
   l.cf = l.T + E;                      // [E] forward increments c_t (log2), careful steps
