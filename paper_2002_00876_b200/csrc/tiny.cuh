@@ -783,9 +783,11 @@ __device__ __forceinline__ void tiny_body(const SmallArgs& a, const int64_t b, f
       a.xout[b] = bad ? qnan() : (float)(XM == 1 ? (double)lz - tot : tot);
     }
   }
-  // every thread waits before it exits: the call completes only after its predecessor, so
-  // everything after it on the stream stays ordered after both
-  if (PROLOGUE && a.early) asm volatile("griddepcontrol.wait;" ::: "memory");
+  // the call completes only after its predecessor, so everything after it on the stream stays
+  // ordered after both: with every write done before the wait (early == 7) one CTA waiting is
+  // enough and the others free their SM slots for the calls behind; otherwise every thread
+  // has waited already
+  if (PROLOGUE && a.early && (a.early != 7 || b == 0)) asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 // The cluster scan's exact fallback: one non-inlined copy of the body, so the cluster
