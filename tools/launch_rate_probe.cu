@@ -1,0 +1,35 @@
+// launch_rate_probe.cu — the floor of back-to-back kernel launches in a CUDA graph: empty
+// kernels of 32 CTAs x 256 threads (cfg2's grid), with and without programmatic dependent
+// launch, and with a 5 us body, per launch (debug tool).
+//   nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o tools/launch_rate_probe tools/launch_rate_probe.cu
+#include <cstdio>
+#include <cuda_runtime.h>
+__global__ void body(long long spin, int trigger) {
+  if (trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const long long t0 = clock64();
+  while (clock64() - t0 < spin) {}
+}
+int main() {
+  cudaStream_t st; cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  for (long long spin : {0LL, 10000LL})
+    for (int pdl = 0; pdl < 2; ++pdl) {
+      const int K = 2000;
+      cudaGraph_t g; cudaGraphExec_t ge;
+      cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
+      for (int k = 0; k < K; ++k) {
+        cudaLaunchConfig_t cfg = {}; cfg.gridDim = dim3(32); cfg.blockDim = dim3(256); cfg.stream = st;
+        cudaLaunchAttribute at[1]; at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1; cfg.attrs = at; cfg.numAttrs = pdl;
+        cudaLaunchKernelEx(&cfg, body, spin, pdl);
+      }
+      cudaStreamEndCapture(st, &g);
+      cudaGraphInstantiate(&ge, g, 0);
+      cudaGraphLaunch(ge, st); cudaStreamSynchronize(st);
+      cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+      cudaEventRecord(e0, st); cudaGraphLaunch(ge, st); cudaEventRecord(e1, st); cudaEventSynchronize(e1);
+      float ms; cudaEventElapsedTime(&ms, e0, e1);
+      printf("spin %lld cycles, pdl=%d: %.3f us per launch (%s)\n", spin, pdl, ms * 1000.f / K,
+             cudaGetErrorString(cudaGetLastError()));
+    }
+  return 0;
+}
