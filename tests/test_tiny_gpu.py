@@ -207,3 +207,58 @@ def test_tiny_early_war_hazard(dev, plan):
         check_marg(m1.cpu().numpy(), mg_x)
         check_logz(l2.cpu().numpy(), lz_y)
         check_marg(m2.cpu().numpy(), mg_y)
+
+
+def test_tiny_early_graph_replay_and_streams(dev, plan):
+    """Overlapping calls captured into a CUDA graph and replayed (the bench's pattern: calls on
+    rotating buffers, some reading what an earlier call in the graph wrote), and calls on two
+    streams joined by events: identical to the same calls made eagerly one after another."""
+    B, N, C = 8, 25, 20
+    pots = [torch.from_numpy(tsgen.potentials(B, N, C, seed=300 + k)).to(dev) for k in range(4)]
+    outs = [torch.empty_like(pots[0]) for _ in range(6)]
+    lzs = [torch.empty(B, device=dev) for _ in range(6)]
+
+    def calls(st):
+        with torch.cuda.stream(st):
+            for k in range(6):
+                src = pots[k % 4] if k < 4 else outs[k - 4]  # calls 4, 5 read calls 0, 1's output
+                tsb.marginals(src, out=outs[k])
+                lzs[k].copy_(tsb.logpartition(src)[0])
+
+    side = torch.cuda.Stream(dev)
+    side.wait_stream(torch.cuda.current_stream(dev))
+    calls(side)
+    torch.cuda.current_stream(dev).wait_stream(side)
+    torch.cuda.synchronize()
+    ref = [o.clone() for o in outs], [z.clone() for z in lzs]
+    for o in outs:
+        o.zero_()
+    g = torch.cuda.CUDAGraph()
+    cap = torch.cuda.Stream(dev)
+    cap.wait_stream(torch.cuda.current_stream(dev))
+    with torch.cuda.graph(g, stream=cap):
+        calls(torch.cuda.current_stream(dev))
+    for _ in range(2):
+        for o in outs:
+            o.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        for a, b in zip(outs, ref[0]):
+            assert torch.equal(a, b)
+        for a, b in zip(lzs, ref[1]):
+            assert torch.equal(a, b)
+    # two streams: the second stream's call reads the first stream's output after an event
+    s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    s1.wait_stream(torch.cuda.current_stream(dev))
+    s2.wait_stream(torch.cuda.current_stream(dev))
+    with torch.cuda.stream(s1):
+        m1, _, _ = tsb.marginals(pots[0])
+        ev = torch.cuda.Event()
+        ev.record(s1)
+        tsb.marginals(pots[1])  # more work behind it on s1
+    with torch.cuda.stream(s2):
+        s2.wait_event(ev)
+        m2, _, _ = tsb.marginals(m1)
+    torch.cuda.synchronize()
+    assert torch.equal(m1, ref[0][0])
+    assert torch.equal(m2, ref[0][4])
