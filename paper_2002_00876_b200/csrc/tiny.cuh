@@ -660,15 +660,16 @@ __device__ __forceinline__ void tiny_body(const SmallArgs& a, const int64_t b, f
   uint64_t* bn = fn + N;
   unsigned* sflag = reinterpret_cast<unsigned*>(bn + N);
 
+  // programmatic dependent launch: the next kernel in the stream may start now (first thing:
+  // the next grid launches only once every CTA of this one has triggered, so the trigger's
+  // position sets the launch-to-launch floor of back-to-back calls)
+  if (PROLOGUE) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   // barriers for every tile / node slot, initialised in parallel before any global access
   for (int64_t k = tid; k < E + 2 * N; k += kTinyThreads)
     mbar_init(k < E ? &ld[k] : (k < E + N ? &fn[k - E] : &bn[k - E - N]), 1);
   if (tid == 0) *sflag = 0u;
   fence_mbar_init();
   if (PROLOGUE) {
-  // programmatic dependent launch: the next kernel in the stream may start its prologue now;
-  // this kernel touches global memory only after the previous grid has completed
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 #ifndef TINY_NO_L2_PREFETCH
   // While the previous grid drains, warm L2 with this sequence's tiles (all N-1 edges, so no
   // input is read yet): a prefetch is only a hint and L2 is the coherence point, so a tile
