@@ -5,12 +5,16 @@
 #include <cstdio>
 #include <cuda_runtime.h>
 __global__ void body(long long spin, int trigger) {
+  extern __shared__ float smem_probe[];
   if (trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (spin < 0) smem_probe[threadIdx.x] = 0.f;  // (never: keeps the dynamic smem alive)
   const long long t0 = clock64();
   while (clock64() - t0 < spin) {}
 }
 int main() {
   cudaStream_t st; cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  cudaFuncSetAttribute(body, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  for (size_t smem : {(size_t)0, (size_t)48 * 1024, (size_t)92 * 1024})
   for (long long spin : {0LL, 10000LL})
     for (int pdl = 0; pdl < 2; ++pdl) {
       const int K = 2000;
@@ -18,6 +22,7 @@ int main() {
       cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
       for (int k = 0; k < K; ++k) {
         cudaLaunchConfig_t cfg = {}; cfg.gridDim = dim3(32); cfg.blockDim = dim3(256); cfg.stream = st;
+        cfg.dynamicSmemBytes = smem;
         cudaLaunchAttribute at[1]; at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         at[0].val.programmaticStreamSerializationAllowed = 1; cfg.attrs = at; cfg.numAttrs = pdl;
         cudaLaunchKernelEx(&cfg, body, spin, pdl);
@@ -28,7 +33,7 @@ int main() {
       cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
       cudaEventRecord(e0, st); cudaGraphLaunch(ge, st); cudaEventRecord(e1, st); cudaEventSynchronize(e1);
       float ms; cudaEventElapsedTime(&ms, e0, e1);
-      printf("spin %lld cycles, pdl=%d: %.3f us per launch (%s)\n", spin, pdl, ms * 1000.f / K,
+      printf("smem %zu KB, spin %lld cycles, pdl=%d: %.3f us per launch (%s)\n", smem >> 10, spin, pdl, ms * 1000.f / K,
              cudaGetErrorString(cudaGetLastError()));
     }
   return 0;
