@@ -39,6 +39,16 @@
 
 namespace tsb {
 
+#ifdef TINY_OCC_TRACE  // (debug, tools/occ_tiny.cu) per-CTA residency records:
+                       // smid, %globaltimer at start / end / after the prepass / after the sweeps
+__device__ unsigned long long g_occ_idx;
+__device__ unsigned long long g_occ_rec[1 << 20][5];
+__device__ __forceinline__ unsigned long long occ_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
 #ifdef TS_PHASE_TIMING
 __device__ long long g_tiny_phase[1024][8];
 __device__ long long g_tiny_steps[2][64];
@@ -664,6 +674,9 @@ __device__ __forceinline__ void tiny_body(const SmallArgs& a, const int64_t b, f
   // the next grid launches only once every CTA of this one has triggered, so the trigger's
   // position sets the launch-to-launch floor of back-to-back calls)
   if (PROLOGUE) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#ifdef TINY_OCC_TRACE
+  const unsigned long long occ_t0 = occ_now();
+#endif
   // barriers for every tile / node slot, initialised in parallel before any global access
   for (int64_t k = tid; k < E + 2 * N; k += kTinyThreads)
     mbar_init(k < E ? &ld[k] : (k < E + N ? &fn[k - E] : &bn[k - E - N]), 1);
@@ -722,6 +735,9 @@ __device__ __forceinline__ void tiny_body(const SmallArgs& a, const int64_t b, f
 #endif
   __syncthreads();
   TPHASE(2);
+#ifdef TINY_OCC_TRACE
+  const unsigned long long occ_t1 = occ_now();
+#endif
 
   const float ones0 = lane < C ? 1.f : (lane == C ? (float)C : 0.f);  // log-one start vector
   double xacc = 0.0;  // fused f1 epilogue: this lane's Σ mu·x
@@ -762,6 +778,9 @@ __device__ __forceinline__ void tiny_body(const SmallArgs& a, const int64_t b, f
   }
   __syncthreads();
   TPHASE(5);
+#ifdef TINY_OCC_TRACE
+  const unsigned long long occ_t2 = occ_now();
+#endif
   if (PROLOGUE && (a.early & 5) == 1) asm volatile("griddepcontrol.wait;" ::: "memory");  // tail writes
   const unsigned fl = (*sflag & TS_F_NONFINITE) ? (unsigned)TS_F_NONFINITE : *sflag;
   if (tid == 0 && a.flags) a.flags[b] = fl;
@@ -789,6 +808,18 @@ __device__ __forceinline__ void tiny_body(const SmallArgs& a, const int64_t b, f
   // enough and the others free their SM slots for the calls behind; otherwise every thread
   // has waited already
   if (PROLOGUE && a.early && (a.early != 7 || b == 0)) asm volatile("griddepcontrol.wait;" ::: "memory");
+#ifdef TINY_OCC_TRACE
+  if (threadIdx.x == 0) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    const unsigned long long i = atomicAdd(&g_occ_idx, 1ull) & ((1 << 20) - 1);
+    g_occ_rec[i][0] = smid;
+    g_occ_rec[i][1] = occ_t0;
+    g_occ_rec[i][2] = occ_now();
+    g_occ_rec[i][3] = occ_t1;
+    g_occ_rec[i][4] = occ_t2;
+  }
+#endif
 }
 
 // The cluster scan's exact fallback: one non-inlined copy of the body, so the cluster

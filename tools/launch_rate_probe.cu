@@ -11,7 +11,46 @@ __global__ void body(long long spin, int trigger) {
   const long long t0 = clock64();
   while (clock64() - t0 < spin) {}
 }
+// a body holding ~120 live registers (a stand-in for fb_tiny's 122)
+__global__ void __launch_bounds__(256, 2) body_regs(long long spin, int trigger) {
+  if (trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  float r[100];
+#pragma unroll
+  for (int i = 0; i < 100; ++i) r[i] = (float)(clock() + i);
+  const long long t0 = clock64();
+  while (clock64() - t0 < spin) {
+#pragma unroll
+    for (int i = 0; i < 100; ++i) r[i] = r[i] * 1.0001f + r[(i + 1) % 100];
+  }
+  float acc = 0.f;
+#pragma unroll
+  for (int i = 0; i < 100; ++i) acc += r[i];
+  if (acc == 12345.f) asm volatile("trap;");
+}
 int main() {
+  {
+    cudaFuncAttributes fa; cudaFuncGetAttributes(&fa, body_regs);
+    printf("body_regs: %d registers\n", fa.numRegs);
+    cudaStream_t st; cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+    for (long long spin : {0LL, 10000LL}) {
+      const int K = 2000;
+      cudaGraph_t g; cudaGraphExec_t ge;
+      cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
+      for (int k = 0; k < K; ++k) {
+        cudaLaunchConfig_t cfg = {}; cfg.gridDim = dim3(32); cfg.blockDim = dim3(256); cfg.stream = st;
+        cudaLaunchAttribute at[1]; at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1; cfg.attrs = at; cfg.numAttrs = 1;
+        cudaLaunchKernelEx(&cfg, body_regs, spin, 1);
+      }
+      cudaStreamEndCapture(st, &g); cudaGraphInstantiate(&ge, g, 0);
+      cudaGraphLaunch(ge, st); cudaStreamSynchronize(st);
+      cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+      cudaEventRecord(e0, st); cudaGraphLaunch(ge, st); cudaEventRecord(e1, st); cudaEventSynchronize(e1);
+      float ms; cudaEventElapsedTime(&ms, e0, e1);
+      printf("regs kernel, spin %lld, pdl=1: %.3f us per launch (%s)\n", spin, ms * 1000.f / K,
+             cudaGetErrorString(cudaGetLastError()));
+    }
+  }
   cudaStream_t st; cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
   cudaFuncSetAttribute(body, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   for (size_t smem : {(size_t)0, (size_t)48 * 1024, (size_t)92 * 1024})
