@@ -262,7 +262,10 @@ TS_API ts_status ts_sample(const ts_chain *c, const float *uniforms, int64_t K, 
  * must not be shared with calls of OTHER entry points while pipelined calls may be in
  * flight.  A change of binding (B, N, C, ws, semiring) or an intervening stream-ordered
  * ts_marginals_host call re-orders the next copy-in after all work on `stream`.
- * ts_set_host_pipeline(0) restores plain stream order. */
+ * ts_set_host_pipeline(0) restores plain stream order.  In that mode, outputs laid out back
+ * to back in host memory (host_logz == host_marg + B (N-1) C^2, host_flags == (uint32_t *)
+ * (host_logz + B)) come back in ONE device-to-host copy (each extra small copy costs a few
+ * microseconds per call on PCIe). */
 TS_API ts_status ts_marginals_host(const ts_chain *host_chain, ts_semiring s, float *host_marg,
                                    float *host_logz, uint32_t *host_flags, void *ws,
                                    size_t ws_bytes, void *stream);

@@ -804,7 +804,7 @@ TS_API size_t ts_workspace_bytes(const ts_chain* c, int op, ts_semiring s) {
       ts_chain dc{Bk, N, C, c->pot, c->lengths};
       cv.take<float>((size_t)(Bk * per));  // pot
       cv.take<int32_t>((size_t)Bk);         // lengths
-      cv.take<float>((size_t)(Bk * per));  // marg
+      cv.take<float>((size_t)(Bk * per + 2 * Bk));  // marg (+ logZ, flags for one copy-back)
       cv.take<float>((size_t)Bk);           // logz
       cv.take<uint32_t>((size_t)Bk);        // flags
       cv.take<char>(op_ws(&dc, TS_OP_MARG, s, nullptr, nullptr, nullptr));
@@ -1370,7 +1370,7 @@ static ts_status host_enqueue(HostPipe* hp, const ts_chain* hc, ts_semiring s, f
     if ((e = cudaStreamWaitEvent(sk, hp->fork, 0)) != cudaSuccess) return cuda_status(e);
     float* d_pot = cv.take<float>(nel);
     int32_t* d_len = cv.take<int32_t>((size_t)Bk);
-    float* d_marg = cv.take<float>(nel);
+    float* d_marg = cv.take<float>(nel + 2 * (size_t)Bk);
     float* d_logz = cv.take<float>((size_t)Bk);
     uint32_t* d_flags = cv.take<uint32_t>((size_t)Bk);
     ts_chain dc{Bk, N, C, nel ? d_pot : nullptr, hc->lengths ? d_len : nullptr};
@@ -1409,6 +1409,20 @@ static ts_status host_compute_d2h(const ts_chain* dc, ts_semiring s, float* d_ma
                                   float* host_marg, float* host_logz, uint32_t* host_flags,
                                   cudaStream_t st) {
   const int64_t B = dc->B, per = (dc->N - 1) * dc->C * dc->C;
+  // host outputs laid out back to back (marg | logZ | flags): the kernel writes logZ / flags
+  // right behind the device marginals (the workspace keeps 2B floats there) and one copy
+  // brings all three back (each small copy costs ~3.5 us per call, tools/pipe_probe2.py)
+  const bool contig = host_logz == host_marg + B * per &&
+                      (!host_flags || reinterpret_cast<float*>(host_flags) == host_logz + B);
+  if (contig) {
+    float* k_logz = d_marg + B * per;
+    uint32_t* k_flags = host_flags ? reinterpret_cast<uint32_t*>(k_logz + B) : nullptr;
+    ts_status r = ts_marginals(dc, s, d_marg, k_logz, k_flags, inner, inner_bytes, st);
+    if (r != TS_OK) return r;
+    const size_t n = (size_t)(B * per + B + (host_flags ? B : 0));
+    const cudaError_t e = cudaMemcpyAsync(host_marg, d_marg, n * 4, cudaMemcpyDeviceToHost, st);
+    return e == cudaSuccess ? TS_OK : cuda_status(e);
+  }
   ts_status r = ts_marginals(dc, s, d_marg, d_logz, d_flags, inner, inner_bytes, st);
   if (r != TS_OK) return r;
   cudaError_t e;
@@ -1432,7 +1446,7 @@ static ts_status host_pipelined(HostPipe* hp, const ts_chain* hc, ts_semiring s,
   Carve cv(ws);
   float* d_pot0 = cv.take<float>(nel);
   int32_t* d_len0 = cv.take<int32_t>((size_t)B);
-  float* d_marg = cv.take<float>(nel);
+  float* d_marg = cv.take<float>(nel + 2 * (size_t)B);
   float* d_logz = cv.take<float>((size_t)B);
   uint32_t* d_flags = cv.take<uint32_t>((size_t)B);
   ts_chain probe{B, N, C, nel ? d_pot0 : nullptr, hc->lengths ? d_len0 : nullptr};

@@ -478,3 +478,32 @@ def test_host_graph_key_covers_kernel_knobs(dev):
     finally:
         tsb.set_tiny(1)
         tsb.set_host_pipeline(True)
+
+
+@pytest.mark.parametrize("with_flags", [True, False])
+def test_host_contiguous_outputs_one_copy(dev, with_flags):
+    """ts_marginals_host with the outputs back to back in one pinned block (marg | logZ |
+    flags): logZ / flags are written behind the device marginals and return in the same copy;
+    back-to-back calls with fresh inputs, BADLEN / EMPTY rows, against the oracle."""
+    B, N, C = 32, 25, 20
+    nel = B * (N - 1) * C * C
+    blk = tsb.host_empty((nel + 2 * B,))
+    marg = blk[:nel].view(B, N - 1, C, C)
+    logz = blk[nel:nel + B]
+    flags = blk[nel + B:].view(torch.int32) if with_flags else None
+    pot = tsb.host_empty((B, N - 1, C, C))
+    lengths = tsb.host_empty((B,), torch.int32)
+    for call in range(5):
+        pot_np = tsgen.potentials(B, N, C, seed=500 + call)
+        pot_np[3] = -np.inf                    # EMPTY
+        len_np = tsgen.random_lengths(B, N, 9 + call).astype(np.int32)
+        len_np[5] = 0                          # BADLEN
+        pot.copy_(torch.from_numpy(pot_np))
+        lengths.copy_(torch.from_numpy(len_np))
+        tsb.marginals_host(pot, marg, logz, flags, lengths_host=lengths, device=dev)
+        torch.cuda.synchronize()
+        lz_ref, mg_ref, fl_ref = oracle.chain_marginals(pot_np, len_np)
+        check_logz(logz.numpy(), lz_ref)
+        check_marg(marg.numpy(), mg_ref)
+        if with_flags:
+            np.testing.assert_array_equal(flags.numpy().astype(np.uint32), fl_ref)
