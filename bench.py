@@ -536,25 +536,31 @@ def run_ours(args):
     hl = hout[B * E * C * C:B * E * C * C + B]
     hf = hout[B * E * C * C + B:].view(torch.int32)
     hws = tsb.Workspace(dev)
-    # warm-up: at least W calls and >= 60 ms of them — host->device DMA on the GPU boxes ramps
-    # from ~90 to ~26 us per 1.2 MB copy over the first ~30 ms of PCIe traffic in a process
+    # warm-up: at least W calls and >= 250 ms of them — host->device DMA on the GPU boxes ramps
+    # from ~90 to ~26 us per 1.2 MB copy over the first tens of ms of PCIe traffic in a process
     # (tools/h2d_warm_probe.py), and the timed region should see the steady state
     e2e_warm, t_w = 0, time.perf_counter()
-    while e2e_warm < max(3, args.warmup) or time.perf_counter() - t_w < 0.06:
+    while e2e_warm < max(3, args.warmup) or time.perf_counter() - t_w < 0.25:
         tsb.marginals_host(hp, hm, hl, hf, device=dev, ws=hws)
         e2e_warm += 1
         if e2e_warm % 32 == 0:
             torch.cuda.synchronize(dev)
     torch.cuda.synchronize(dev)
-    ctx.barrier()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(e2e_steps):
-        tsb.marginals_host(hp, hm, hl, hf, device=dev, ws=hws)
-    e1.record(stream)
-    torch.cuda.synchronize(dev)
-    e_ms = ctx.max_over_ranks([e0.elapsed_time(e1)])[0]
+
+    def e2e_region():
+        ctx.barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(e2e_steps):
+            tsb.marginals_host(hp, hm, hl, hf, device=dev, ws=hws)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        return ctx.max_over_ranks([e0.elapsed_time(e1)])[0]
+
+    # three regions of e2e_steps calls each (the PCIe path of the GPU boxes is noisy): median
+    e2e_ms = [e2e_region() for _ in range(3)]
+    e_ms = statistics.median(e2e_ms)
     e2e_value = world * e2e_steps * cfg.tokens / (e_ms / 1e3)
 
     side = side_configs(ctx, args) if args.side else {}
@@ -603,7 +609,9 @@ def run_ours(args):
                     "d2h_bytes_per_step": B * E * C * C * 4 + 8 * B,
                     "api": "ts_marginals_host (ts_host_alloc page-locked host buffers, outputs "
                            "back to back; H2D, kernels, D2H inside every call)",
-                    "steps": e2e_steps, "warmup_calls": e2e_warm},
+                    "steps": e2e_steps, "warmup_calls": e2e_warm,
+                    "regions_us_per_step": [round(x / e2e_steps * 1e3, 2) for x in e2e_ms],
+                    "pipeline": "three-stage (copy-in / kernels / copy-back on library streams)"},
             "gpu_launches": K * launches_per_step,
             "clocks": sampler.summary(),
             "side": side,

@@ -274,9 +274,13 @@ TS_API ts_status ts_marginals_host(const ts_chain *host_chain, ts_semiring s, fl
  * 0 = always enqueue eagerly. */
 TS_API void ts_set_host_graphs(int on);
 
-/* Debug/testing: 1 (default) = the cross-call copy pipeline of ts_marginals_host for
- * single-chunk payloads (see there), 0 = every call fully ordered on its stream. */
-TS_API void ts_set_host_pipeline(int on);
+/* Debug/testing: the cross-call pipeline of ts_marginals_host for single-chunk payloads
+ * (see there).  2 (default) = three stages: call k+1's copy-in, call k's kernels and call
+ * k-1's copy-back run concurrently on library streams (input and output staging
+ * double-buffered; `stream` waits for each call's copy-back); 1 = the two-stream copy pipeline
+ * (copy-in on a library stream, kernels and copy-back on `stream`); 0 = every call fully
+ * ordered on its stream. */
+TS_API void ts_set_host_pipeline(int mode);
 
 /* Debug/testing: leaf chunk summaries of the time-chunked scan for 64 < C <= 128 run on
  * the tensor cores (tcgen05 kind::tf32): 3 = 3xTF32 split (default), 1 = one TF32 pass,

@@ -287,9 +287,12 @@ def get_tc_summary() -> int:
     return int(_lib.load().ts_get_tc_summary())
 
 
-def set_host_pipeline(enable: bool) -> None:
-    """Debug knob: cross-call copy pipeline of marginals_host for single-chunk payloads."""
-    _lib.load().ts_set_host_pipeline(1 if enable else 0)
+def set_host_pipeline(mode) -> None:
+    """Debug knob: cross-call pipeline of marginals_host for single-chunk payloads: 2 (default,
+    or True) = three stages on library streams, 1 = two-stream copy pipeline, 0 (or False) =
+    every call fully ordered on its stream."""
+    m = 2 if mode is True else (0 if mode is False else int(mode))
+    _lib.load().ts_set_host_pipeline(m)
 
 
 def set_host_graphs(enable: bool) -> None:

@@ -623,7 +623,7 @@ int host_chunks(int64_t B, int64_t per_seq_floats) {
 }
 
 std::atomic<int> g_host_graphs{1};
-std::atomic<int> g_host_pipeline{1};
+std::atomic<int> g_host_pipeline{2};  // 2 = three-stage, 1 = two-stream, 0 = stream order
 
 struct HostKey {
   int64_t B, N, C;
@@ -670,6 +670,14 @@ struct HostPipe {
   // staging buffers; ev_in[p] = copy-in done, ev_done[p] = the call that used buffer p done
   cudaStream_t cin;
   cudaEvent_t ev_in[2], ev_done[2];
+  // three-stage pipeline (pipeline mode 2): copy-in on `cin`, kernels on `ck`, copy-back on
+  // `cout`, input and output staging double-buffered; e3_in / e3_k / e3_out[p] = the copy-in,
+  // kernels, copy-back of the last call that used buffer set p
+  cudaStream_t ck, cout;
+  cudaEvent_t e3_in[2], e3_k[2], e3_out[2], e3_fork;
+  bool p3_primed[2] = {false, false};
+  int p3_parity = 0;
+  int64_t p3_sig[5] = {0, 0, 0, 0, 0};
   // the previous call (any path) and its stream: a call on another stream orders after it,
   // since all calls share the device staging buffers and the inner workspace
   cudaEvent_t ev_last;
@@ -718,10 +726,16 @@ HostPipe* host_pipe() {
     bool ok = cudaEventCreateWithFlags(&p->fork, cudaEventDisableTiming) == cudaSuccess &&
               cudaEventCreateWithFlags(&p->ev_last, cudaEventDisableTiming) == cudaSuccess &&
               cudaStreamCreateWithFlags(&p->cap, cudaStreamNonBlocking) == cudaSuccess &&
-              cudaStreamCreateWithFlags(&p->cin, cudaStreamNonBlocking) == cudaSuccess;
+              cudaStreamCreateWithFlags(&p->cin, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaStreamCreateWithFlags(&p->ck, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaStreamCreateWithFlags(&p->cout, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaEventCreateWithFlags(&p->e3_fork, cudaEventDisableTiming) == cudaSuccess;
     for (int k = 0; k < 2 && ok; ++k)
       ok = cudaEventCreateWithFlags(&p->ev_in[k], cudaEventDisableTiming) == cudaSuccess &&
-           cudaEventCreateWithFlags(&p->ev_done[k], cudaEventDisableTiming) == cudaSuccess;
+           cudaEventCreateWithFlags(&p->ev_done[k], cudaEventDisableTiming) == cudaSuccess &&
+           cudaEventCreateWithFlags(&p->e3_in[k], cudaEventDisableTiming) == cudaSuccess &&
+           cudaEventCreateWithFlags(&p->e3_k[k], cudaEventDisableTiming) == cudaSuccess &&
+           cudaEventCreateWithFlags(&p->e3_out[k], cudaEventDisableTiming) == cudaSuccess;
     for (int k = 0; k < kHostMaxChunks && ok; ++k)
       ok = cudaStreamCreateWithFlags(&p->side[k], cudaStreamNonBlocking) == cudaSuccess &&
            cudaEventCreateWithFlags(&p->join[k], cudaEventDisableTiming) == cudaSuccess;
@@ -812,6 +826,7 @@ TS_API size_t ts_workspace_bytes(const ts_chain* c, int op, ts_semiring s) {
     if (K == 1) {  // second input staging buffer of the cross-call pipeline
       cv.take<float>((size_t)(B * per));
       cv.take<int32_t>((size_t)B);
+      cv.take<float>((size_t)(B * per + 2 * B));  // second output staging (three-stage mode)
     }
     return cv.off;
   }
@@ -1524,11 +1539,103 @@ static ts_status host_pipelined(HostPipe* hp, const ts_chain* hc, ts_semiring s,
   return TS_OK;
 }
 
+// Three-stage pipeline across calls (single-chunk payloads, pipeline mode 2): call k's
+// copy-in (`cin`), kernels (`ck`) and copy-back (`cout`) run on library streams into buffer set
+// p = k % 2 (input staging and output staging [marg | logZ | flags] each double-buffered), so
+// call k+1's copy-in, call k's kernels and call k-1's copy-back overlap (PCIe full duplex);
+// `stream` waits for the call's copy-back.  The copy-in of buffer set p waits for the kernels
+// of the call that last read it, the kernels for the copy-back of the call that last read its
+// output staging (tools/pipe_probe3.py: 42 vs 51 us per call at cfg2).
+static ts_status host_pipe3(HostPipe* hp, const ts_chain* hc, ts_semiring s, float* host_marg,
+                            float* host_logz, uint32_t* host_flags, void* ws, cudaStream_t st) {
+  const int64_t B = hc->B, N = hc->N, C = hc->C, per = (N - 1) * C * C;
+  const size_t nel = (size_t)(B * per);
+  Carve cv(ws);
+  float* d_pot0 = cv.take<float>(nel);
+  int32_t* d_len0 = cv.take<int32_t>((size_t)B);
+  float* d_out0 = cv.take<float>(nel + 2 * (size_t)B);
+  cv.take<float>((size_t)B);     // (logz / flags of the two-stream path)
+  cv.take<uint32_t>((size_t)B);
+  ts_chain probe{B, N, C, nel ? d_pot0 : nullptr, hc->lengths ? d_len0 : nullptr};
+  const size_t inner_bytes = op_ws(&probe, TS_OP_MARG, s, nullptr, nullptr, nullptr);
+  void* inner = cv.take<char>(inner_bytes);
+  float* d_pot1 = cv.take<float>(nel);
+  int32_t* d_len1 = cv.take<int32_t>((size_t)B);
+  float* d_out1 = cv.take<float>(nel + 2 * (size_t)B);
+  cudaError_t e;
+  const int64_t sig[5] = {B, N, C, (int64_t)reinterpret_cast<uintptr_t>(ws), (int64_t)s};
+  if (std::memcmp(sig, hp->p3_sig, sizeof sig) != 0) {
+    std::memcpy(hp->p3_sig, sig, sizeof sig);
+    hp->p3_primed[0] = hp->p3_primed[1] = false;
+  }
+  const int p = hp->p3_parity;
+  hp->p3_parity ^= 1;
+  float* d_pot = p ? d_pot1 : d_pot0;
+  int32_t* d_len = p ? d_len1 : d_len0;
+  float* d_out = p ? d_out1 : d_out0;
+  const bool primed = hp->p3_primed[p];
+  if (!primed) {  // first use of this set (or a new layout): after everything on `stream`
+    if ((e = cudaEventRecord(hp->e3_fork, st)) != cudaSuccess) return cuda_status(e);
+    if ((e = cudaStreamWaitEvent(hp->cin, hp->e3_fork, 0)) != cudaSuccess) return cuda_status(e);
+    if ((e = cudaStreamWaitEvent(hp->ck, hp->e3_fork, 0)) != cudaSuccess) return cuda_status(e);
+  } else if ((e = cudaStreamWaitEvent(hp->cin, hp->e3_k[p], 0)) != cudaSuccess) {
+    return cuda_status(e);
+  }
+  // 1. copy-in
+  if (nel && (e = cudaMemcpyAsync(d_pot, hc->pot, nel * 4, cudaMemcpyHostToDevice, hp->cin)) !=
+                 cudaSuccess)
+    return cuda_status(e);
+  if (hc->lengths && (e = cudaMemcpyAsync(d_len, hc->lengths, (size_t)B * 4,
+                                          cudaMemcpyHostToDevice, hp->cin)) != cudaSuccess)
+    return cuda_status(e);
+  if ((e = cudaEventRecord(hp->e3_in[p], hp->cin)) != cudaSuccess) return cuda_status(e);
+  // 2. kernels (logZ and flags land right behind the device marginals)
+  if ((e = cudaStreamWaitEvent(hp->ck, hp->e3_in[p], 0)) != cudaSuccess) return cuda_status(e);
+  if (primed && (e = cudaStreamWaitEvent(hp->ck, hp->e3_out[p], 0)) != cudaSuccess)
+    return cuda_status(e);
+  ts_chain dc{B, N, C, nel ? d_pot : nullptr, hc->lengths ? d_len : nullptr};
+  float* k_logz = d_out + nel;
+  uint32_t* k_flags = reinterpret_cast<uint32_t*>(k_logz + B);
+  const ts_status r = ts_marginals(&dc, s, d_out, k_logz, k_flags, inner, inner_bytes, hp->ck);
+  if (r != TS_OK) return r;
+  if ((e = cudaEventRecord(hp->e3_k[p], hp->ck)) != cudaSuccess) return cuda_status(e);
+  // 3. copy-back: one copy when the host outputs are back to back
+  if ((e = cudaStreamWaitEvent(hp->cout, hp->e3_k[p], 0)) != cudaSuccess) return cuda_status(e);
+  const bool contig = host_logz == host_marg + nel &&
+                      (!host_flags || reinterpret_cast<float*>(host_flags) == host_logz + B);
+  if (contig) {
+    const size_t n = nel + (size_t)B + (host_flags ? (size_t)B : 0);
+    if ((e = cudaMemcpyAsync(host_marg, d_out, n * 4, cudaMemcpyDeviceToHost, hp->cout)) != cudaSuccess)
+      return cuda_status(e);
+  } else {
+    if (nel && (e = cudaMemcpyAsync(host_marg, d_out, nel * 4, cudaMemcpyDeviceToHost, hp->cout)) !=
+                   cudaSuccess)
+      return cuda_status(e);
+    if ((e = cudaMemcpyAsync(host_logz, k_logz, (size_t)B * 4, cudaMemcpyDeviceToHost, hp->cout)) !=
+        cudaSuccess)
+      return cuda_status(e);
+    if (host_flags && (e = cudaMemcpyAsync(host_flags, k_flags, (size_t)B * 4, cudaMemcpyDeviceToHost,
+                                           hp->cout)) != cudaSuccess)
+      return cuda_status(e);
+  }
+  if ((e = cudaEventRecord(hp->e3_out[p], hp->cout)) != cudaSuccess) return cuda_status(e);
+  // 4. the caller's stream sees the results once it is past this event
+  if ((e = cudaStreamWaitEvent(st, hp->e3_out[p], 0)) != cudaSuccess) return cuda_status(e);
+  hp->p3_primed[p] = true;
+  return TS_OK;
+}
+
 // ts_marginals_host body, under hp->mu, after the cross-stream ordering.
 ts_status marginals_host_locked(HostPipe* hp, const ts_chain* hc, ts_semiring s,
                                 float* host_marg, float* host_logz, uint32_t* host_flags,
                                 void* ws, size_t ws_bytes, cudaStream_t st) {
-  if (g_host_pipeline.load() && host_chunks(hc->B, (hc->N - 1) * hc->C * hc->C) == 1)
+  const bool one_chunk = host_chunks(hc->B, (hc->N - 1) * hc->C * hc->C) == 1;
+  if (g_host_pipeline.load() == 2 && one_chunk) {
+    hp->primed[0] = hp->primed[1] = false;  // (the two-stream path's buffers are reused here)
+    return host_pipe3(hp, hc, s, host_marg, host_logz, host_flags, ws, st);
+  }
+  hp->p3_primed[0] = hp->p3_primed[1] = false;
+  if (g_host_pipeline.load() == 1 && one_chunk)
     return host_pipelined(hp, hc, s, host_marg, host_logz, host_flags, ws, ws_bytes, st);
   // a stream-ordered call: the next pipelined call must order its copy-in after it again
   hp->primed[0] = hp->primed[1] = false;
@@ -1600,7 +1707,7 @@ TS_API ts_status ts_marginals_host(const ts_chain* hc, ts_semiring s, float* hos
 }
 
 TS_API void ts_set_host_graphs(int on) { g_host_graphs.store(on ? 1 : 0); }
-TS_API void ts_set_host_pipeline(int on) { g_host_pipeline.store(on ? 1 : 0); }
+TS_API void ts_set_host_pipeline(int mode) { g_host_pipeline.store(mode <= 0 ? 0 : (mode == 1 ? 1 : 2)); }
 
 TS_API void ts_set_tc_summary(int mode) { tsb::set_tc_summary(mode); }
 TS_API int ts_get_tc_summary(void) { return tsb::get_tc_summary(); }

@@ -339,7 +339,7 @@ def test_host_buffers_end_to_end(dev, shape, graphs):
         tsb.set_host_graphs(True)
 
 
-@pytest.mark.parametrize("pipeline", [True, False])
+@pytest.mark.parametrize("pipeline", [2, 1, 0])
 def test_host_pipeline_back_to_back(dev, pipeline):
     """Cross-call copy pipeline of ts_marginals_host (single-chunk payloads): 6 calls
     enqueued back to back WITHOUT synchronising, alternating between two input/output
@@ -507,3 +507,33 @@ def test_host_contiguous_outputs_one_copy(dev, with_flags):
         check_marg(marg.numpy(), mg_ref)
         if with_flags:
             np.testing.assert_array_equal(flags.numpy().astype(np.uint32), fl_ref)
+
+
+def test_host_pipeline_modes_interleaved(dev):
+    """Host calls switching pipeline mode (three-stage, two-stream, stream-ordered) and
+    output layout (back to back, separate) between calls, enqueued without synchronising on
+    the same workspace: every result matches the oracle."""
+    B, N, C = 32, 25, 20
+    nel = B * (N - 1) * C * C
+    calls = []
+    try:
+        for k, mode in enumerate([2, 2, 1, 2, 0, 2, 1, 1, 2]):
+            tsb.set_host_pipeline(mode)
+            pot_np = tsgen.potentials(B, N, C, seed=900 + k)
+            pot = tsb.host_empty((B, N - 1, C, C))
+            pot.copy_(torch.from_numpy(pot_np))
+            if k % 2:
+                blk = tsb.host_empty((nel + 2 * B,))
+                outs = (blk[:nel].view(B, N - 1, C, C), blk[nel:nel + B], blk[nel + B:].view(torch.int32))
+            else:
+                outs = (tsb.host_empty((B, N - 1, C, C)), tsb.host_empty((B,)), tsb.host_empty((B,), torch.int32))
+            tsb.marginals_host(pot, *outs, device=dev)
+            calls.append((pot_np, pot, outs))
+        torch.cuda.synchronize()
+    finally:
+        tsb.set_host_pipeline(True)
+    for pot_np, _, (m, l, f) in calls:
+        lz_ref, mg_ref, fl_ref = oracle.chain_marginals(pot_np)
+        check_logz(l.numpy(), lz_ref)
+        check_marg(m.numpy(), mg_ref)
+        np.testing.assert_array_equal(f.numpy().astype(np.uint32), fl_ref)
