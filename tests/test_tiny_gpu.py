@@ -262,3 +262,34 @@ def test_tiny_early_graph_replay_and_streams(dev, plan):
     torch.cuda.synchronize()
     assert torch.equal(m1, ref[0][0])
     assert torch.equal(m2, ref[0][4])
+
+
+def _mixed_run(early, pots, feat):
+    tsb.set_tiny_early(early)
+    try:
+        outs = []
+        x = pots[0]
+        for k in range(10):
+            m, lz, fl = tsb.marginals(pots[k % 3])
+            h = tsb.entropy(pots[(k + 1) % 3])[0]
+            ex = tsb.expectation(pots[(k + 2) % 3], feat)[0]
+            lz2 = tsb.logpartition(x)[0]
+            x = m  # the next logpartition reads these marginals
+            outs += [m, lz, fl, h, ex, lz2]
+        torch.cuda.synchronize()
+        return [o.clone() for o in outs]
+    finally:
+        tsb.set_tiny_early(True)
+
+
+def test_tiny_early_mixed_entry_points(dev, plan):
+    """Back-to-back marginals / entropy / expectation (fused epilogue variants) / logZ-only
+    calls, some reading what an earlier call wrote, none synchronised: identical to the same
+    sequence with every call waiting first."""
+    B, N, C = 16, 25, 20
+    pots = [torch.from_numpy(tsgen.potentials(B, N, C, seed=60 + k)).to(dev) for k in range(3)]
+    feat = torch.from_numpy(tsgen.potentials(B, N, C, seed=99)).to(dev)
+    a = _mixed_run(True, pots, feat)
+    b = _mixed_run(False, pots, feat)
+    for x, y in zip(a, b):
+        assert torch.equal(torch.nan_to_num(x.float(), nan=7.0), torch.nan_to_num(y.float(), nan=7.0))
