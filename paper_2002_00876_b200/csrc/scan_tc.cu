@@ -11,7 +11,13 @@
 //
 // D = (Ahat o w) . X runs on tcgen05 kind::tf32 as 3xTF32 (hi.hi + hi.lo + lo.hi, fp32
 // accumulate in TMEM; measured max relative error 2.9e-6 per 128^3 product vs 3.7e-4 for a
-// single TF32 pass, tools/tc_probe.cu), then each row is renormalised by its sum s_m
+// single TF32 pass, tools/tc_probe.cu).  Default shift (predicted): one scalar per tile, r_i =
+// R_u = T_u for every row, so w = 1 and X_u = e^(l_u - T_u) with T_u = the previous tile's
+// max (tile 0: its own) — the producers need ONE pass per tile and the epilogue never waits for
+// them; a tile whose max is off the prediction by more than 2^40 either way, or with a finite
+// entry 2^40 below it, flags the chunk for the exact kernel (TC_ROW_SHIFT builds the per-row
+// shifts of the formula above in a second pass: 3.51 vs 3.17 us per step).  Each row of D is
+// then renormalised by its sum s_m
 // (Ahat_{u+1} = D / c_m, off_m += R_u + ln c_m, fp64) with the LAGGED row scale c_m = the
 // previous step's row sum s_m (any positive scale is exact), so the epilogue converts D_u to
 // A_{u+1} in one pass, block by block, releasing each 32-column block of A to the MMA issuer
@@ -70,8 +76,8 @@ constexpr int kOffBlo = 4 * kBlk;           // [4][16 KB] tf32-lo
 constexpr int kOffStg = 8 * kBlk;           // [kPW][16 KB / kPW x 4] raw staging (kPR rows each)
 constexpr int kOffW = 12 * kBlk;            // float wbuf[2][132]: w[128], R (natural)
 constexpr int kOffRs = kOffW + 2 * 132 * 4; // float rsc[4][32] row maxes of the current tile
-constexpr int kOffRp = kOffRs + 4 * 32 * 4; // float Rp[2][kPW] per-warp maxes
-constexpr int kOffBar = kOffRp + 64;        // mbarriers
+constexpr int kOffRp = kOffRs + 4 * 32 * 4; // float Rp[4][kPW] per-warp maxes (and mins)
+constexpr int kOffBar = kOffRp + 4 * kPW * 4;  // mbarriers
 // bars: full[4] empty[4] stg[kPW] wready[2] dfull aready[4] (one per 32-column block of A)
 constexpr int kBarFull = 0, kBarEmpty = 4, kBarStg = 8, kBarW = 8 + kPW, kBarD = kBarW + 2,
               kBarA = kBarD + 1;
@@ -202,6 +208,123 @@ __global__ void __launch_bounds__(kTcThreads, 1) summary_tc_kernel(ScanArgs a) {
                      : "memory");
 #endif
     }
+#ifndef TC_ROW_SHIFT
+    // Single pass per tile with a PREDICTED shift: X_u = 2^((l - T_u) log2 e) with one scalar
+    // T_u per tile = the previous tile's max (tile 0: its own max, one extra pass), so there are
+    // no row weights (w = 1) and the epilogue never waits for this tile's pass; the tile's max
+    // and finite min are gathered in the same pass and a prediction off by more than 2^40
+    // either way (or a finite entry 2^40 below the shift) flags the chunk for the exact kernel.
+    float Tp = 0.f;
+    for (int u = 0; u < n; ++u) {
+      if (rows > 0) tc_wait(&bars[kBarStg + pw], (uint32_t)(u & 1), 1, u);
+      TCP(u, 0);
+      if (u == 0) {  // tile 0: exact max
+        float m = neg_inf();
+#pragma unroll
+        for (int rr = 0; rr < kPR; ++rr)
+#pragma unroll
+          for (int jb = 0; jb < 4; ++jb) {
+            const int j = 32 * jb + lane;
+            m = fmax_nan(m, (rr < rows && j < C) ? stg[rr * C + j] : neg_inf());
+          }
+        m = warp_max(m);
+        if (lane == 0) Rp[kPW + pw] = m;
+        named_bar(1, 32 * kPW);
+        float R = Rp[kPW];
+#pragma unroll
+        for (int q = 1; q < kPW; ++q) R = fmaxf(R, Rp[kPW + q]);
+        Tp = (R == neg_inf() || !(R == R) || R == pos_inf()) ? 0.f : R;
+      }
+      const float Tcur = Tp, tl = Tp * kLog2e;
+      // B stage p free (the MMA of tile u-1 is done with it)?  Then publish this tile's shift.
+      if (u > 0) tc_wait(&bars[kBarEmpty + p], (uint32_t)((u - 1) & 1), 2, u);
+      TCP(u, 2);
+      if (pw == 0 && lane == 0) wbuf[(u & 1) * 132 + 128] = Tp;
+      mbar_arrive(&bars[kBarW + (u & 1)]);
+      float mx = neg_inf(), mnf = pos_inf();
+      float lvn[16];
+#pragma unroll
+      for (int x = 0; x < 16; ++x) {
+        const int rr = x & 3, j = 32 * (x >> 2) + lane;
+        lvn[x] = (rr < rows && j < C) ? stg[rr * C + j] : neg_inf();
+      }
+#pragma unroll kP2Unroll
+      for (int kg = 0; kg < kPR / 4; ++kg) {
+        float lv[16];
+#pragma unroll
+        for (int x = 0; x < 16; ++x) lv[x] = lvn[x];
+        if (kg + 1 < kPR / 4) {
+#pragma unroll
+          for (int x = 0; x < 16; ++x) {
+            const int rr = 4 * (kg + 1) + (x & 3), j = 32 * (x >> 2) + lane;
+            lvn[x] = (rr < rows && j < C) ? stg[rr * C + j] : neg_inf();
+          }
+        }
+#pragma unroll
+        for (int x = 0; x < 16; ++x) {
+          mx = fmax_nan(mx, lv[x]);
+          mnf = fminf(mnf, lv[x] == neg_inf() ? pos_inf() : lv[x]);
+        }
+#pragma unroll
+        for (int jb = 0; jb < 4; ++jb) {
+          const int j = 32 * jb + lane;
+          float e[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) e[q] = ex2(fmaf(lv[4 * jb + q], kLog2e, -tl));
+          float4 h, l;
+          tc::split_tf32(e[0], h.x, l.x);
+          tc::split_tf32(e[1], h.y, l.y);
+          tc::split_tf32(e[2], h.z, l.z);
+          tc::split_tf32(e[3], h.w, l.w);
+          const uint32_t off = bstage_off(j, kg0 + kg);
+          *reinterpret_cast<float4*>(bhi + off) = h;
+          if (NP == 3) *reinterpret_cast<float4*>(blo + off) = l;
+        }
+      }
+      TCP(u, 4);
+      tc::fence_async_smem();
+      __syncwarp();
+      TCP(u, 5);
+      if (lane == 0 && rows > 0 && u + 1 < n)
+        bulk_load(smem + kOffStg + pw * kStg, potb + (t0 + u + 1) * CC + (int64_t)i0 * C,
+                  blk_bytes, &bars[kBarStg + pw]);
+#ifndef TC_NO_L2_AHEAD
+      if (lane == 0 && rows > 0 && u + kTcAhead < n)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                         potb + (t0 + u + kTcAhead) * CC + (int64_t)i0 * C),
+                     "r"(blk_bytes)
+                     : "memory");
+#endif
+      tc::fence_async_smem();
+      if (pw == 0 && lane == 0) TCT(u, 7);
+      TCP(u, 3);
+      mbar_arrive(&bars[kBarFull + p]);
+      // this tile's max (the next tile's shift) and gates
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        mx = fmax_nan(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        mnf = fminf(mnf, __shfl_xor_sync(0xffffffffu, mnf, o));
+      }
+      bad |= (mx != mx) | (mx == pos_inf());
+      if (lane == 0) {
+        Rp[(u & 1) * kPW + pw] = mx;
+        Rp[2 * kPW + (u & 1) * kPW + pw] = mnf;
+      }
+      named_bar(1, 32 * kPW);
+      float M = Rp[(u & 1) * kPW], Mn = Rp[2 * kPW + (u & 1) * kPW];
+#pragma unroll
+      for (int q = 1; q < kPW; ++q) {
+        M = fmaxf(M, Rp[(u & 1) * kPW + q]);
+        Mn = fminf(Mn, Rp[2 * kPW + (u & 1) * kPW + q]);
+      }
+      if (M != neg_inf() && M == M && M != pos_inf()) {
+        const float dM = (M - Tp) * kLog2e;
+        tiny |= (dM > 40.f) | (dM < -40.f);  // the prediction was off by more than 2^40
+        Tp = M;
+      }
+      tiny |= (Mn != pos_inf()) & ((Mn - Tcur) * kLog2e < kTinyXtc);
+    }
+#else
     for (int u = 0; u < n; ++u) {
       // ---- tile u, rows i0.., columns j = 32 jb + lane; pass 1: row max and finite min ----
       if (rows > 0) tc_wait(&bars[kBarStg + pw], (uint32_t)(u & 1), 1, u);
@@ -336,6 +459,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) summary_tc_kernel(ScanArgs a) {
       TCP(u, 3);
       mbar_arrive(&bars[kBarFull + p]);
     }
+#endif  // !TC_ROW_SHIFT
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&misc[1], 1u);
     if (__any_sync(0xffffffffu, tiny) && lane == 0) atomicOr(&misc[1], 2u);
   } else if (warp == kMmaWarp) {
@@ -379,11 +503,18 @@ __global__ void __launch_bounds__(kTcThreads, 1) summary_tc_kernel(ScanArgs a) {
     double off = 0.0;
     bool dead = (m >= C);
     bool tinyp = false;
-    // A_0 = diag(w^(0)) (the identity start, weighted by tile 0's row weights)
+    // A_0 = I (the identity start; with the TC_ROW_SHIFT variant diag(w^(0)), tile 0's row
+    // weights)
+#ifdef TC_ROW_SHIFT
     tc_wait(&bars[kBarW + 0], 0u, 4, 0);
+#endif
     {
       float wh, wl;
+#ifndef TC_ROW_SHIFT
+      tc::split_tf32(dead ? 0.f : 1.f, wh, wl);
+#else
       tc::split_tf32(dead ? 0.f : wbuf[m], wh, wl);
+#endif
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         uint32_t vh[32], vl[32];
@@ -415,13 +546,19 @@ __global__ void __launch_bounds__(kTcThreads, 1) summary_tc_kernel(ScanArgs a) {
       tc_wait(&bars[kBarD], (uint32_t)(u & 1), 5, u);
       tc::fence_after();
       if (tid == 0) TCT(u, 3);
+#ifndef TC_ROW_SHIFT
+      tc_wait(&bars[kBarW + (u & 1)], (uint32_t)((u >> 1) & 1), 6, u);  // this tile's shift
+#endif
       const float Ru = wbuf[(u & 1) * 132 + 128];
       if (u + 1 < n) {
         const int nb = (u + 1) & 1;
         if (tid == 0) TCT(u, 4);
+#ifdef TC_ROW_SHIFT
         tc_wait(&bars[kBarW + nb], (uint32_t)(((u + 1) >> 1) & 1), 6, u);
+#endif
         if (tid == 0) TCT(u, 5);
         const float* w = wbuf + nb * 132;
+        (void)w;
         float s4[4] = {0.f, 0.f, 0.f, 0.f};
         float pmin = pos_inf();
 #pragma unroll
@@ -435,7 +572,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) summary_tc_kernel(ScanArgs a) {
             const float p = x * inv;
             if (p > 0.f) pmin = fminf(pmin, p);
             float h, l;
+#ifndef TC_ROW_SHIFT
+            tc::split_tf32(p, h, l);
+#else
             tc::split_tf32(p * w[32 * c + q], h, l);
+#endif
             vh[q] = __float_as_uint(h);
             vl[q] = __float_as_uint(l);
           }
