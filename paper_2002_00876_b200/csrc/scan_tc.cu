@@ -561,6 +561,36 @@ __global__ void __launch_bounds__(kTcThreads, 1) summary_tc_kernel(ScanArgs a) {
         (void)w;
         float s4[4] = {0.f, 0.f, 0.f, 0.f};
         float pmin = pos_inf();
+#if !defined(TC_EPI_NOPIPE) && !defined(TC_ROW_SHIFT)
+        // blocks double-buffered in registers: block c+1's TMEM load is in flight while block
+        // c is converted (hi in place of D, lo beside it)
+        uint32_t va[32], vb[32], vl[32];
+        tc::ld32_async(tD + lb, va);
+        tc::wait_ld32(va);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t(&v)[32] = (c & 1) ? vb : va;
+          uint32_t(&vn)[32] = (c & 1) ? va : vb;
+          if (c + 1 < 4) tc::ld32_async(tD + lb + 32 * (c + 1), vn);
+#pragma unroll
+          for (int q = 0; q < 32; ++q) {
+            const float x = __uint_as_float(v[q]);
+            s4[q & 3] += x;
+            const float p = x * inv;
+            if (p > 0.f) pmin = fminf(pmin, p);
+            float h, l;
+            tc::split_tf32(p, h, l);
+            v[q] = __float_as_uint(h);
+            vl[q] = __float_as_uint(l);
+          }
+          tc::st32(tAh + lb + 32 * c, v);
+          if (NP == 3) tc::st32(tAl + lb + 32 * c, vl);
+          tc::wait_st();
+          tc::fence_before();
+          mbar_arrive(&bars[kBarA + c]);
+          if (c + 1 < 4) tc::wait_ld32(vn);
+        }
+#else
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           uint32_t v[32], vh[32], vl[32];
@@ -586,6 +616,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) summary_tc_kernel(ScanArgs a) {
           tc::fence_before();
           mbar_arrive(&bars[kBarA + c]);
         }
+#endif
         const float s = (s4[0] + s4[1]) + (s4[2] + s4[3]);
         if (!dead) off += (double)Ru + kLn2 * (double)Rprev_ls;
         dead |= !(s > 0.f);

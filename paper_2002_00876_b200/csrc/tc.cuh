@@ -103,7 +103,23 @@ __device__ __forceinline__ void ld32(uint32_t taddr, uint32_t (&v)[32]) {
       : TSB_R8(0), TSB_R8(8), TSB_R8(16), TSB_R8(24)
       : "r"(taddr));
 }
+// Split form for software pipelining: ld32_async issues the load, wait_ld32 completes it;
+// the wait names the destination registers as in/out operands, so no use of them can be
+// scheduled before it.
+__device__ __forceinline__ void ld32_async(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : TSB_R8(0), TSB_R8(8), TSB_R8(16), TSB_R8(24)
+      : "r"(taddr));
+}
 #undef TSB_R8
+#define TSB_RW8(i) "+r"(v[i]), "+r"(v[i + 1]), "+r"(v[i + 2]), "+r"(v[i + 3]), "+r"(v[i + 4]), \
+                   "+r"(v[i + 5]), "+r"(v[i + 6]), "+r"(v[i + 7])
+__device__ __forceinline__ void wait_ld32(uint32_t (&v)[32]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" : TSB_RW8(0), TSB_RW8(8), TSB_RW8(16), TSB_RW8(24)::"memory");
+}
+#undef TSB_RW8
 #define TSB_W8(i) "r"(v[i]), "r"(v[i + 1]), "r"(v[i + 2]), "r"(v[i + 3]), "r"(v[i + 4]), \
                   "r"(v[i + 5]), "r"(v[i + 6]), "r"(v[i + 7])
 __device__ __forceinline__ void st32(uint32_t taddr, const uint32_t (&v)[32]) {
