@@ -141,3 +141,20 @@ def test_auto_plan_per_rank_cfg3_keeps_meet64(dev, G):
     tsgen.fill_torch(pot, cfg)
     tsb.marginals(pot)
     assert tsb.last_kernel() == "meet64_kernel"
+
+
+@pytest.mark.parametrize("jump", [8.0, 30.0, 120.0])
+def test_tensor_core_predicted_shift(dev, jump):
+    """The tensor-core summaries shift each tile by the previous tile's max (a prediction):
+    tiles whose level jumps by +-jump nats from one edge to the next (30: within the 2^40
+    tolerance, no gate; 120: the prediction gate sends the chunk to the exact kernel), whole
+    -inf tiles (at a chunk start and inside), and a chunk whose first tile is masked except one
+    entry — all within the BASELINE gates of the fp64 oracle."""
+    B, N, C = 3, 160, 128
+    pot = tsgen.potentials(B, N, C, seed=int(jump))
+    lvl = np.where(np.arange(N - 1) % 2 == 0, 0.0, jump).astype(np.float32)
+    pot = (pot + lvl[None, :, None, None]).astype(np.float32)
+    pot[1, 40] = -np.inf                    # a whole masked tile inside a chunk
+    pot[2, 0] = -np.inf                     # the first tile of the first chunk ...
+    pot[2, 0, 3, 5] = 1.0                   # ... except one entry
+    check_plan(pot, None, dev, [40, 17])
