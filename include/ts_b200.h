@@ -362,7 +362,11 @@ TS_API void ts_set_wide_ring(int enable);
  * its inputs before waiting for a still-running earlier call on the stream (programmatic
  * dependent launch), so consecutive calls overlap everything but their global writes — when
  * the library has not recorded a recent call whose outputs overlap this call's pot / lengths
- * (then it waits before reading, as with 0).  Results are identical either way. */
+ * (then it waits before reading, as with 0).  Results are identical either way.
+ * Contract: only this library's kernels are assumed to trigger programmatic dependents
+ * (griddepcontrol.launch_dependents / cudaTriggerProgrammaticLaunchCompletion); if a caller's
+ * own kernel that does so writes a buffer a following ts_* call reads, without an event or
+ * other stream operation in between, set 0. */
 TS_API void ts_set_tiny_early(int enable);
 
 /* Debug/testing knob (process-global): 1 (default) runs ts_marginals for C = 64 with one
